@@ -1,0 +1,347 @@
+"""Throughput of the B200 batched environment step (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--scenario c3] [--envs B]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference ...     # the reference's CPU step (oracle port)
+
+Workload (BASELINE.json configs[2], the metric's config): C3 = 10v10
+heterogeneous roles on the 2L2B2S terrain map, 262,144 environments in total,
+sharded over the ranks (strong scaling).  Ally team on the in-engine random
+controller, enemy heuristic-medium (the reference bench's ``_scripted`` rule,
+rollout.py:360-366); auto-reset on; episodes truncate at t=400.
+
+* ``value``: env-steps/s of the whole job, state and outputs resident in
+  HBM, CUDA-event timed over K steps (max over ranks).  Each step writes
+  ~8.1 GB of observations, so every timed step streams far more than L2.
+* ``e2e``: the same metric through the trainer API (``bindings.step``)
+  with host buffers: int64 actions copied from pinned host memory every step
+  (ally team external), rewards + terminated + truncated copied back.
+* ``roofline``: the step kernel's algorithmic HBM bytes (SURVEY.md §8(d):
+  4·N·obs_dim + 4·gdim + 4N + 7N + 3 + 8N + 2·(89N+40) per env-step) per
+  launch ÷ its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
+* ``cpu_baseline``: the oracle port of the reference step (numpy, same
+  numerics as the reference) on a bounded sample, 1 host thread.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SCENARIOS = {"c1": "c1_3v3", "c2": "c2_10v10", "c3": "c3_10v10_terrain", "c4": "c4_50v50"}
+DEFAULT_ENVS = {"c1": 256, "c2": 65536, "c3": 262144, "c4": 131072}
+WORKLOAD = {
+    "c1": "C1 3v3 farmers, open map, random ally vs heuristic-medium enemy",
+    "c2": "C2 10v10 heterogeneous roles (melee/ranged/support), random vs heuristic-medium",
+    "c3": "C3 10v10 heterogeneous roles on the 2L2B2S terrain map (lava, bush, swamp), "
+          "random vs heuristic-medium",
+    "c4": "C4 50v50 large battle, random vs heuristic-medium",
+}
+
+
+def algorithmic_bytes(N: int, Z: int) -> int:
+    """SURVEY.md §8(d) compulsory bytes per env-step."""
+    D = 15 + 17 * (N - 1) + 8 * Z
+    G = 15 * N + 8 * Z
+    return 4 * N * D + 4 * G + 4 * N + 7 * N + 3 + 8 * N + 2 * (89 * N + 40)
+
+
+def load_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}",
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 4 + k and r[4 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference(scenario_key: str, envs: int, steps: int, warmup: int, seed: int = 0) -> dict:
+    """The reference's CPU step (numpy oracle port) on a bounded sample."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+    import tabx_oracle as orc
+
+    from paper_2602_01665_b200.rng import lane_seeds
+    from paper_2602_01665_b200.scenario import builtin_scenario
+
+    sc = builtin_scenario(SCENARIOS[scenario_key]).scripted()
+    sim = orc.OracleBatchSim([sc] * envs, lane_seeds(seed, envs), auto_reset=True)
+    for _ in range(warmup):
+        sim.step(None)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sim.step(None)
+    dt = time.perf_counter() - t0
+    return {"env_steps_per_s": envs * steps / dt, "seconds": dt, "envs": envs, "steps": steps,
+            "n_units": len(sc.units), "numpy": np.__version__}
+
+
+def run_reference_arm(args) -> int:
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    envs = args.cpu_envs
+    r = cpu_reference(args.scenario, envs, max(args.steps, 1), max(args.warmup, 1))
+    sc_units = r["n_units"]
+    v = r["env_steps_per_s"]
+    line = {
+        "metric": "env_steps_per_s", "value": v, "unit": "env-steps/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * r["seconds"] / r["steps"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (scenario JSON, seeded lanes)", "impl": "reference",
+        "agent_steps_per_s": v * sc_units,
+        "config": {"workload": WORKLOAD[args.scenario], "scenario": SCENARIOS[args.scenario],
+                   "envs": envs, "host_threads": 1},
+        "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "port",
+                         "sample": f"{envs} envs x {r['steps']} steps (+{max(args.warmup, 1)} "
+                                   f"warm-up), oracle/tabx_oracle.py numpy {r['numpy']}"},
+        "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_gpu_arm(args) -> int:
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_01665_b200 import bindings
+    from paper_2602_01665_b200.rng import lane_seeds
+    from paper_2602_01665_b200.scenario import builtin_scenario, save_scenario
+    from paper_2602_01665_b200.sim import BatchSim
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    total = args.envs or DEFAULT_ENVS[args.scenario]
+    per = total // world
+    first = rank * per
+    if rank == world - 1:
+        per = total - first
+    base = builtin_scenario(SCENARIOS[args.scenario])
+    sc = base.scripted()
+    N, Z = sc.max_units, sc.max_zones
+    seeds = lane_seeds(args.seed, per, first)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- device-resident throughput (value + roofline)
+    sim = BatchSim([sc] * per, seeds, auto_reset=True, device=dev, interactions=False)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(args.warmup):
+        sim.step(None)
+    barrier()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t0.record(stream)
+        for k in range(args.steps):
+            starts[k].record(stream)
+            sim.step(None)
+            ends[k].record(stream)
+        t1.record(stream)
+        barrier()
+    elapsed_ms = max_over_ranks(t0.elapsed_time(t1))
+    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    value = total * args.steps / (elapsed_ms / 1000.0)
+    stats = sim.episode_stats()
+    if world > 1:
+        vec = torch.tensor([stats[k] for k in ("episodes", "ally_wins", "first_kill_ally",
+                                               "truncation_ties", "sum_length", "sum_return",
+                                               "eliminations")], dtype=torch.float64, device=dev)
+        dist.all_reduce(vec)  # NCCL over NVLink: the per-window episode-statistics reduction
+        stats = dict(zip(("episodes", "ally_wins", "first_kill_ally", "truncation_ties",
+                          "sum_length", "sum_return", "eliminations"), vec.tolist()))
+    sim.close()
+    del sim
+    torch.cuda.empty_cache()
+
+    # ---------------- end-to-end through the trainer API with host buffers
+    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    doc = save_scenario(base).encode()  # ally external, enemy heuristic-medium
+    h = bindings.make_batch(doc, per, args.seed, device=dev, first_lane=first,
+                            interactions=False, final_observations=True)
+    gen = np.random.default_rng(1234 + rank)
+    pinned = [torch.from_numpy(gen.integers(0, 5, size=(per, N), dtype=np.int64)).pin_memory()
+              for _ in range(4)]  # moves/rotate: always legal, no host mask round trip
+    rew_h = torch.empty((per, N), dtype=torch.float32).pin_memory()
+    term_h = torch.empty(per, dtype=torch.bool).pin_memory()
+    trunc_h = torch.empty(per, dtype=torch.bool).pin_memory()
+
+    def e2e_step(k):
+        a = pinned[k % len(pinned)].to(dev, non_blocking=True)
+        obs, glob, rew, term, trunc, mask = bindings.step(h, a)
+        rew_h.copy_(rew, non_blocking=True)
+        term_h.copy_(term, non_blocking=True)
+        trunc_h.copy_(trunc, non_blocking=True)
+        stream.synchronize()
+
+    for k in range(args.warmup):
+        e2e_step(k)
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for k in range(e2e_steps):
+        e2e_step(k)
+    e1.record(stream)
+    barrier()
+    wall = time.perf_counter() - w0
+    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), 1000.0 * wall))
+    e2e_value = total * e2e_steps / (e2e_ms / 1000.0)
+    h.sim.close()
+
+    # ---------------- CPU baseline (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = cpu_reference(args.scenario, args.cpu_envs, args.cpu_steps, 1)
+        cpu = {"value": r["env_steps_per_s"], "unit": "env-steps/s", "cores": 1, "kind": "port",
+               "sample": f"{r['envs']} envs x {r['steps']} steps (+1 warm-up), "
+                         f"oracle/tabx_oracle.py numpy {r['numpy']}, {r['seconds']:.1f} s"}
+
+    if rank == 0:
+        peaks = load_peaks()
+        peak = peaks.get("hbm_gbs", 6451.2)
+        bytes_per = algorithmic_bytes(N, Z)
+        kern_avg = statistics.mean(kern_ms)
+        achieved = bytes_per * per / (kern_avg / 1000.0) / 1e9
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", f"traffic_{args.scenario}.json")
+        if os.path.exists(prof):
+            with open(prof) as fh:
+                traffic = json.load(fh).get("bytes_per_launch")
+        line = {
+            "metric": "env_steps_per_s", "value": value, "unit": "env-steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (scenario JSON, seeded lanes)",
+            "agent_steps_per_s": value * len(sc.units),
+            "config": {"workload": WORKLOAD[args.scenario], "scenario": SCENARIOS[args.scenario],
+                       "envs": total, "envs_per_gpu": per, "n_units": N, "n_zones": Z,
+                       "obs_dim": sim_dims(N, Z)[0], "global_dim": sim_dims(N, Z)[1],
+                       "parallelism": f"env-shard x{world}",
+                       "l2": "inputs larger than L2: every step writes "
+                             f"{4 * N * sim_dims(N, Z)[0] * per / 1e9:.1f} GB of observations",
+                       "e2e_workload": "bindings.step, ally external: int64 actions H2D from "
+                                       "pinned host, rewards/terminated/truncated D2H"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "bytes_per_env_step": bytes_per, "kernel_ms_avg": kern_avg,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "e2e": {"value": e2e_value, "unit": "env-steps/s",
+                    "h2d_bytes_per_step": per * N * 8,
+                    "d2h_bytes_per_step": per * N * 4 + 2 * per},
+            "gpu_launches": args.steps,
+            "clocks": clk.summary(),
+            "episode_stats": stats,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def sim_dims(N, Z):
+    return 15 + 17 * (N - 1) + 8 * Z, 15 * N + 8 * Z
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("tabx", "reference"), default="tabx")
+    ap.add_argument("--scenario", choices=sorted(SCENARIOS), default="c3")
+    ap.add_argument("--envs", type=int, default=0, help="total environments (all ranks)")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-envs", type=int, default=256)
+    ap.add_argument("--cpu-steps", type=int, default=40)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args(argv)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,257 @@
+/*
+ * tabx.h -- C ABI of the B200-native batched environment step.
+ *
+ * Drop-in boundary for the reference engine's batch path.  Each entry point
+ * replaces one piece of the reference's Python interface:
+ *
+ *   tabx_create        BatchSim.__init__            pkg/src/skirmish/environment.py:472-484
+ *                      (+ make_batch lane seeding  pkg/bindings/src/skirmish_bindings/__init__.py:51-75)
+ *   tabx_init_output   init_output / BatchSim.last  environment.py:351-374
+ *   tabx_step          BatchSim.step -> step_kernel environment.py:500-519, :207-348
+ *                      (+ bindings step            bindings/.../__init__.py:89-123)
+ *   tabx_reset_env     BatchSim.reset_env           environment.py:490-498
+ *   tabx_export_state  BatchSim.sim (SimArrays)     arrays.py:45-132
+ *   tabx_import_state  (parity injection into SimArrays)
+ *   tabx_get_error     ActionMaskError              environment.py:166-178, core.py:34
+ *   tabx_episode_stats rollout.summarize inputs     rollout.py:122-147
+ *
+ * Conventions: plain pointers and sizes only.  Every pointer inside
+ * tabx_outputs / tabx_state is a DEVICE pointer on the handle's device;
+ * tabx_config / seeds are HOST pointers.  All work is enqueued on the
+ * handle's stream; nothing synchronises except tabx_get_error /
+ * tabx_episode_stats.  Every function returns TABX_OK (0) or an error code;
+ * tabx_last_error() describes the last failure on the calling thread.
+ * A handle must not be shared between threads (bindings/.../__init__.py:9-10).
+ */
+#ifndef TABX_H_
+#define TABX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TABX_ABI_VERSION 1
+
+#define TABX_MAX_UNITS 256
+#define TABX_MAX_ZONES 32
+#define TABX_MAX_CONFIGS 256
+#define TABX_NUM_ACTIONS 7
+#define TABX_OWN_DIM 15
+#define TABX_OTHER_DIM 17
+#define TABX_ZONE_DIM 8
+#define TABX_NUM_STATS 8
+
+/* status codes */
+#define TABX_OK 0
+#define TABX_E_ARGUMENT 1     /* bad pointer / size / index                 */
+#define TABX_E_CUDA 2         /* CUDA runtime failure (see tabx_last_error) */
+#define TABX_E_ACTION_MASK 3  /* an external action violated the mask       */
+#define TABX_E_SHAPE 4        /* config capacities differ from the handle's */
+#define TABX_E_ALIGNMENT 5    /* observation buffer not 16-byte aligned     */
+#define TABX_E_CAPACITY 6     /* too many distinct configs                  */
+
+/* controller ids (core.py:138) */
+#define TABX_CTRL_EXTERNAL 0
+#define TABX_CTRL_HEURISTIC 1
+#define TABX_CTRL_RANDOM 2
+
+/* zone ids (arrays.py:24-27) */
+#define TABX_ZONE_NONE 0
+#define TABX_ZONE_LAVA 1
+#define TABX_ZONE_BUSH 2
+#define TABX_ZONE_SWAMP 3
+
+/*
+ * One scenario resolved to a device template: static unit columns, spawn
+ * state, team controllers, physics and zones (arrays.py:244-321).  Angles are
+ * radians and cos(sight_angle/2) is precomputed on the host with numpy so the
+ * spawn state is bit-identical to the reference's fill_env.  Padding slots
+ * (i >= number of configured units, i < n_units) carry the reference's
+ * padding values (max_health 1, radius 0, mass 1, inv_mass 1, cos_half 1).
+ */
+typedef struct tabx_config {
+  int32_t n_units;       /* capacity N = max_units, 1..TABX_MAX_UNITS */
+  int32_t n_zones;       /* capacity Z = max_zones, 0..TABX_MAX_ZONES */
+  int32_t max_steps;
+  int32_t enable_noop;
+  int32_t controller[2]; /* per team, TABX_CTRL_* */
+  double epsilon[2];     /* heuristic exploration rate per team */
+  double aggressive[2];  /* heuristic kiting threshold per team */
+  double dt, restitution, slop, correction, rot_step, boundary_coeff, reveal_duration;
+  double field_w, field_h;
+  uint8_t active[TABX_MAX_UNITS];
+  uint8_t team[TABX_MAX_UNITS];
+  uint8_t kinematic[TABX_MAX_UNITS];
+  uint8_t role_assassin[TABX_MAX_UNITS];
+  uint8_t role_ranger[TABX_MAX_UNITS];
+  uint8_t role_healer[TABX_MAX_UNITS];
+  double max_health[TABX_MAX_UNITS];
+  double radius[TABX_MAX_UNITS];
+  double mass[TABX_MAX_UNITS];
+  double inv_mass[TABX_MAX_UNITS];
+  double speed[TABX_MAX_UNITS];
+  double damage[TABX_MAX_UNITS];
+  double attack_range[TABX_MAX_UNITS];
+  double cooldown[TABX_MAX_UNITS];
+  double sight_angle[TABX_MAX_UNITS];
+  double sight_cos_half[TABX_MAX_UNITS];
+  double sight_range[TABX_MAX_UNITS];
+  double spawn_x[TABX_MAX_UNITS];
+  double spawn_y[TABX_MAX_UNITS];
+  double spawn_heading[TABX_MAX_UNITS];
+  int32_t zone_type[TABX_MAX_ZONES];
+  double zone_cx[TABX_MAX_ZONES];
+  double zone_cy[TABX_MAX_ZONES];
+  double zone_ax[TABX_MAX_ZONES];
+  double zone_ay[TABX_MAX_ZONES];
+  double zone_effect[TABX_MAX_ZONES];
+} tabx_config;
+
+/*
+ * Per-step outputs (BatchOutput, environment.py:113-136), caller-owned
+ * device buffers written in place; NULL skips a field.  observations and
+ * global_state are float32 (the reference computes float64; values are the
+ * float64 results rounded to nearest float32).  Bool arrays are one byte.
+ * final_* rows are written only for lanes that auto-reset this step
+ * (reset_mask[b] = 1); other rows are left untouched, so the reference's
+ * final_observations equals where(reset_mask, final_observations, observations).
+ */
+typedef struct tabx_outputs {
+  float* observations;        /* [B, N, obs_dim]          */
+  float* global_state;        /* [B, global_dim]          */
+  float* rewards;             /* [B, N]                   */
+  uint8_t* action_mask;       /* [B, N, 7]                */
+  uint8_t* terminated;        /* [B]                      */
+  uint8_t* truncated;         /* [B]                      */
+  uint8_t* done;              /* [B]                      */
+  double* dense_reward;       /* [B]                      */
+  int64_t* actions;           /* [B, N] executed actions  */
+  uint8_t* interactions;      /* [B, N, N]                */
+  int64_t* winner;            /* [B]                      */
+  int64_t* reason;            /* [B]                      */
+  int64_t* first_kill;        /* [B]                      */
+  double* episode_return;     /* [B]                      */
+  int64_t* episode_length;    /* [B]                      */
+  float* final_observations;  /* [B, N, obs_dim]          */
+  float* final_global_state;  /* [B, global_dim]          */
+  uint8_t* reset_mask;        /* [B]                      */
+} tabx_outputs;
+
+/*
+ * Dynamic state in the reference's SimArrays dtypes (arrays.py:45-117),
+ * device pointers, for export (parity checks) and import (state injection).
+ * vis/atk are [B, N, N] bools (row = observer / attacker).
+ */
+typedef struct tabx_state {
+  uint64_t* seed;       /* [B]       */
+  int64_t* episode;     /* [B]       */
+  int64_t* t;           /* [B]       */
+  double* pos;          /* [B, N, 2] */
+  double* heading;      /* [B, N]    */
+  double* vel;          /* [B, N, 2] */
+  double* imp_dv;       /* [B, N, 2] */
+  double* health;       /* [B, N]    */
+  double* cooldown;     /* [B, N]    */
+  double* reveal;       /* [B, N]    */
+  uint8_t* alive;       /* [B, N]    */
+  double* prev_gap;     /* [B]       */
+  double* ep_return;    /* [B]       */
+  uint8_t* done;        /* [B]       */
+  uint8_t* terminated;  /* [B]       */
+  uint8_t* truncated;   /* [B]       */
+  int64_t* winner;      /* [B]       */
+  int64_t* reason;      /* [B]       */
+  int64_t* first_kill;  /* [B]       */
+  double* mem_pos;      /* [B, N, 2] */
+  uint8_t* mem_valid;   /* [B, N]    */
+  uint8_t* vis;         /* [B, N, N] */
+  uint8_t* atk;         /* [B, N, N] */
+  int32_t* config;      /* [B] index into the handle's config table */
+} tabx_state;
+
+/* First offending external action in row-major (env, unit) order. */
+typedef struct tabx_error {
+  int32_t code;   /* TABX_OK or TABX_E_ACTION_MASK */
+  int32_t unit;
+  int64_t env;
+  int64_t action;
+} tabx_error;
+
+typedef struct tabx_handle tabx_handle;
+
+int tabx_abi_version(void);
+const char* tabx_last_error(void);
+
+/* Size of obs/global rows for capacities N, Z (perception.py:40-49). */
+int32_t tabx_obs_dim(int32_t n_units, int32_t n_zones);
+int32_t tabx_global_dim(int32_t n_units, int32_t n_zones);
+
+/*
+ * Create a batch of `batch` lanes on `device`.  configs[0..n_configs) share
+ * n_units / n_zones; env_config[b] (host, may be NULL = all 0) picks lane b's
+ * config; seeds[b] (host) is lane b's episode seed.  Lanes are spawned
+ * immediately; call tabx_init_output to produce the first observations.
+ * stream is a cudaStream_t (NULL = legacy default stream).
+ */
+int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* env_config,
+                const uint64_t* seeds, int64_t batch, int32_t auto_reset, int32_t device,
+                void* stream, tabx_handle** out);
+int tabx_destroy(tabx_handle* h);
+int tabx_set_stream(tabx_handle* h, void* stream);
+int tabx_dims(const tabx_handle* h, int64_t* batch, int32_t* n_units, int32_t* n_zones,
+              int32_t* obs_dim, int32_t* global_dim);
+
+/* init_output: refresh caches, prev_gap, observations, masks for all lanes. */
+int tabx_init_output(tabx_handle* h, const tabx_outputs* out);
+
+/*
+ * One step of every lane.  actions: device int64 [B, N] or NULL (the
+ * reference's step(None): non-scripted units NOOP).  When actions are given
+ * and a team is external, they are validated first; on a violation no lane
+ * is mutated and tabx_get_error reports TABX_E_ACTION_MASK.  Asynchronous.
+ */
+int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out);
+
+/*
+ * reset_env(b, config, seed): respawn lane b (optionally with a new config,
+ * appended to the handle's config table, and/or a new seed), then run
+ * init_output for the whole batch into `out` (environment.py:490-498).
+ */
+int tabx_reset_env(tabx_handle* h, int64_t b, const tabx_config* config, uint64_t seed,
+                   int32_t has_seed, const tabx_outputs* out);
+
+/*
+ * Respawn every lane with new seeds (host [B]) and episode counters 0, and
+ * zero the statistics: the bindings' reset() (bindings/.../__init__.py:78-86).
+ * Call tabx_init_output afterwards.
+ */
+int tabx_respawn_all(tabx_handle* h, const uint64_t* seeds, const int32_t* env_config);
+
+int tabx_export_state(tabx_handle* h, const tabx_state* dst);
+int tabx_import_state(tabx_handle* h, const tabx_state* src);
+
+/* Synchronises the stream; reports (and with clear != 0 clears) the action error. */
+int tabx_get_error(tabx_handle* h, tabx_error* err, int32_t clear);
+
+/*
+ * Episode statistics accumulated on device since creation or the last reset
+ * (host double[TABX_NUM_STATS], synchronises): episodes, ally_wins,
+ * first_kill_ally, truncation_ties, sum_length, sum_return, eliminations,
+ * env_steps.  dst_device (may be NULL) receives the same vector on device for
+ * an NCCL all-reduce.
+ */
+int tabx_episode_stats(tabx_handle* h, double* dst_host, double* dst_device, int32_t reset);
+
+/* sizeof of the ABI structs, so bindings can check their mirrors. */
+int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state);
+
+/* Test hook: libm-equal sin/cos of n device doubles (tabx_math.cuh). */
+int tabx_debug_sincos(const double* x, double* s, double* c, int64_t n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TABX_H_ */

@@ -1,0 +1,91 @@
+"""Build the in-tree CUDA extension ``_tabx.so`` for sm_100a.
+
+    python -m paper_2602_01665_b200.build
+
+Each translation unit is compiled in parallel with
+``nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false``
+(``-fmad=false``: no product may be fused that the reference's numpy rounds),
+then linked into one shared object next to this file.  Objects are cached
+by source hash under ``build/`` so unchanged units are not recompiled.
+"""
+from __future__ import annotations
+
+import hashlib
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "_tabx.so")
+BUILD = os.path.join(ROOT, "build", "tabx")
+
+UNITS = ["tabx_lane_w1.cu", "tabx_lane_w2.cu", "tabx_lane_w4.cu", "tabx_lane_w8.cu",
+         "tabx_aux.cu", "tabx_capi.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+         "-Xcompiler", "-ffp-contract=off", "-I", os.path.join(ROOT, "include")]
+
+
+def nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _digest() -> str:
+    h = hashlib.sha256()
+    for name in sorted(os.listdir(CSRC)):
+        with open(os.path.join(CSRC, name), "rb") as fh:
+            h.update(name.encode())
+            h.update(fh.read())
+    with open(os.path.join(ROOT, "include", "tabx.h"), "rb") as fh:
+        h.update(fh.read())
+    h.update(" ".join(ARCH + FLAGS).encode())
+    return h.hexdigest()[:16]
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    tag = _digest()
+    stamp = OUT + ".stamp"
+    if not force and os.path.exists(OUT) and os.path.exists(stamp):
+        with open(stamp) as fh:
+            if fh.read().strip() == tag:
+                return OUT
+    os.makedirs(BUILD, exist_ok=True)
+    cc = nvcc()
+    procs = []
+    objs = []
+    for unit in UNITS:
+        obj = os.path.join(BUILD, f"{unit}.{tag}.o")
+        objs.append(obj)
+        if os.path.exists(obj) and not force:
+            continue
+        cmd = [cc, *ARCH, *FLAGS, "-c", os.path.join(CSRC, unit), "-o", obj]
+        if verbose:
+            cmd += ["-Xptxas", "-v"]
+        procs.append((unit, subprocess.Popen(cmd, stdout=subprocess.PIPE,
+                                             stderr=subprocess.STDOUT, text=True)))
+    failed = []
+    for unit, p in procs:
+        out, _ = p.communicate()
+        if verbose and out:
+            print(out)
+        if p.returncode != 0:
+            failed.append((unit, out))
+    if failed:
+        msg = "\n".join(f"--- {u}\n{o}" for u, o in failed)
+        raise RuntimeError(f"nvcc failed:\n{msg}")
+    tmp = OUT + ".tmp"
+    subprocess.check_call([cc, *ARCH, "-shared", "-o", tmp, *objs])
+    os.replace(tmp, OUT)
+    with open(stamp, "w") as fh:
+        fh.write(tag + "\n")
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -1,0 +1,266 @@
+// Auxiliary kernels: action validation, spawn, state export/import,
+// statistics reduction, libm test hook, and the lane-kernel dispatcher.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tabx_device.cuh"
+#include "tabx_math.cuh"
+
+namespace tabx {
+
+cudaError_t launch_lanes_w1(const Params& P, int sm_count, cudaStream_t stream, int* grid);
+cudaError_t launch_lanes_w2(const Params& P, int sm_count, cudaStream_t stream, int* grid);
+cudaError_t launch_lanes_w4(const Params& P, int sm_count, cudaStream_t stream, int* grid);
+cudaError_t launch_lanes_w8(const Params& P, int sm_count, cudaStream_t stream, int* grid);
+
+// External action validation (environment.py:166-178): first offender in
+// row-major order is latched with atomicMin before any lane mutates.
+__global__ void validate_kernel(const int64_t* __restrict__ actions, DevState st,
+                                const tabx_config* __restrict__ cfgs, int64_t B, int N,
+                                Sync* sync) {
+  const int64_t n = B * N;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = u / N;
+    const int i = (int)(u - b * N);
+    if (st.flags[b] & F_DONE) continue;
+    const tabx_config* C = cfgs + st.cfg[b];
+    if (!C->active[i] || !(st.ubits[u] & U_ALIVE)) continue;
+    if (C->controller[C->team[i] ? 1 : 0] != TABX_CTRL_EXTERNAL) continue;
+    const int64_t a = actions[u];
+    bool ok;
+    if (a < 0 || a >= TABX_NUM_ACTIONS) {
+      ok = false;
+    } else if (a == A_ATTACK) {
+      ok = st.cooldown[u] <= 0.0;
+    } else if (a == A_NOOP) {
+      ok = C->enable_noop != 0;
+    } else {
+      ok = true;
+    }
+    if (!ok) atomicMin(&sync->err_index, (unsigned long long)u);
+  }
+}
+
+// fill_env for lanes [b0, b1) (arrays.py:244-321); also used at creation.
+__global__ void spawn_kernel(DevState st, const tabx_config* __restrict__ cfgs, int64_t b0,
+                             int64_t b1, int N, int W, int reset_stats) {
+  for (int64_t b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
+    const tabx_config* C = cfgs + st.cfg[b];
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const int64_t u = b * N + i;
+      if (C->active[i]) {
+        st.pos[u] = make_double2(C->spawn_x[i], C->spawn_y[i]);
+        st.heading[u] = C->spawn_heading[i];
+        st.health[u] = C->max_health[i];
+        st.ubits[u] = U_ALIVE;
+      } else {
+        st.ubits[u] = 0;
+      }
+      st.vel[u] = make_double2(0.0, 0.0);
+      st.imp_dv[u] = make_double2(0.0, 0.0);
+      st.cooldown[u] = 0.0;
+      st.reveal[u] = 0.0;
+      st.mem_pos[u] = make_double2(0.0, 0.0);
+      for (int k = 0; k < W; ++k) {
+        st.vis[u * W + k] = 0u;
+        st.atk[u * W + k] = 0u;
+      }
+    }
+    if (threadIdx.x == 0) {
+      st.t[b] = 0;
+      st.prev_gap[b] = 0.0;
+      st.ep_return[b] = 0.0;
+      st.flags[b] = 0;
+      st.winner[b] = -1;
+      st.reason[b] = R_NONE;
+      st.first_kill[b] = -1;
+      if (reset_stats) {
+        st.st_episodes[b] = st.st_wins[b] = st.st_fk_ally[b] = st.st_ties[b] = st.st_elims[b] = 0;
+        st.st_len[b] = 0;
+        st.st_ret[b] = 0.0;
+      }
+    }
+  }
+}
+
+__global__ void export_kernel(DevState st, tabx_state d, int64_t B, int N, int W) {
+  const int64_t n = B * N;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = u / N;
+    const int i = (int)(u - b * N);
+    if (i == 0) {
+      if (d.seed) d.seed[b] = st.seed[b];
+      if (d.episode) d.episode[b] = st.episode[b];
+      if (d.t) d.t[b] = st.t[b];
+      if (d.prev_gap) d.prev_gap[b] = st.prev_gap[b];
+      if (d.ep_return) d.ep_return[b] = st.ep_return[b];
+      if (d.done) d.done[b] = (st.flags[b] & F_DONE) ? 1 : 0;
+      if (d.terminated) d.terminated[b] = (st.flags[b] & F_TERM) ? 1 : 0;
+      if (d.truncated) d.truncated[b] = (st.flags[b] & F_TRUNC) ? 1 : 0;
+      if (d.winner) d.winner[b] = st.winner[b];
+      if (d.reason) d.reason[b] = st.reason[b];
+      if (d.first_kill) d.first_kill[b] = st.first_kill[b];
+      if (d.config) d.config[b] = st.cfg[b];
+    }
+    if (d.pos) { d.pos[2 * u] = st.pos[u].x; d.pos[2 * u + 1] = st.pos[u].y; }
+    if (d.heading) d.heading[u] = st.heading[u];
+    if (d.vel) { d.vel[2 * u] = st.vel[u].x; d.vel[2 * u + 1] = st.vel[u].y; }
+    if (d.imp_dv) { d.imp_dv[2 * u] = st.imp_dv[u].x; d.imp_dv[2 * u + 1] = st.imp_dv[u].y; }
+    if (d.health) d.health[u] = st.health[u];
+    if (d.cooldown) d.cooldown[u] = st.cooldown[u];
+    if (d.reveal) d.reveal[u] = st.reveal[u];
+    if (d.alive) d.alive[u] = (st.ubits[u] & U_ALIVE) ? 1 : 0;
+    if (d.mem_pos) { d.mem_pos[2 * u] = st.mem_pos[u].x; d.mem_pos[2 * u + 1] = st.mem_pos[u].y; }
+    if (d.mem_valid) d.mem_valid[u] = (st.ubits[u] & U_MEMV) ? 1 : 0;
+    for (int j = 0; j < N; ++j) {
+      const uint32_t vb = (st.vis[u * W + (j >> 5)] >> (j & 31)) & 1u;
+      const uint32_t ab = (st.atk[u * W + (j >> 5)] >> (j & 31)) & 1u;
+      if (d.vis) d.vis[u * N + j] = (uint8_t)vb;
+      if (d.atk) d.atk[u * N + j] = (uint8_t)ab;
+    }
+  }
+}
+
+__global__ void import_kernel(DevState st, tabx_state s, int64_t B, int N, int W) {
+  const int64_t n = B * N;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = u / N;
+    const int i = (int)(u - b * N);
+    if (i == 0) {
+      if (s.seed) st.seed[b] = s.seed[b];
+      if (s.episode) st.episode[b] = s.episode[b];
+      if (s.t) st.t[b] = (int32_t)s.t[b];
+      if (s.prev_gap) st.prev_gap[b] = s.prev_gap[b];
+      if (s.ep_return) st.ep_return[b] = s.ep_return[b];
+      if (s.done && s.terminated && s.truncated)
+        st.flags[b] = (s.done[b] ? F_DONE : 0) | (s.terminated[b] ? F_TERM : 0) |
+                      (s.truncated[b] ? F_TRUNC : 0);
+      if (s.winner) st.winner[b] = (int8_t)s.winner[b];
+      if (s.reason) st.reason[b] = (int8_t)s.reason[b];
+      if (s.first_kill) st.first_kill[b] = (int8_t)s.first_kill[b];
+      if (s.config) st.cfg[b] = s.config[b];
+    }
+    if (s.pos) st.pos[u] = make_double2(s.pos[2 * u], s.pos[2 * u + 1]);
+    if (s.heading) st.heading[u] = s.heading[u];
+    if (s.vel) st.vel[u] = make_double2(s.vel[2 * u], s.vel[2 * u + 1]);
+    if (s.imp_dv) st.imp_dv[u] = make_double2(s.imp_dv[2 * u], s.imp_dv[2 * u + 1]);
+    if (s.health) st.health[u] = s.health[u];
+    if (s.cooldown) st.cooldown[u] = s.cooldown[u];
+    if (s.reveal) st.reveal[u] = s.reveal[u];
+    if (s.mem_pos) st.mem_pos[u] = make_double2(s.mem_pos[2 * u], s.mem_pos[2 * u + 1]);
+    if (s.alive && s.mem_valid)
+      st.ubits[u] = (s.alive[u] ? U_ALIVE : 0) | (s.mem_valid[u] ? U_MEMV : 0);
+    if (s.vis && s.atk) {
+      for (int k = 0; k < W; ++k) {
+        uint32_t vw = 0, aw = 0;
+        for (int jj = 0; jj < 32; ++jj) {
+          const int j = (k << 5) + jj;
+          if (j >= N) break;
+          if (s.vis[u * N + j]) vw |= 1u << jj;
+          if (s.atk[u * N + j]) aw |= 1u << jj;
+        }
+        st.vis[u * W + k] = vw;
+        st.atk[u * W + k] = aw;
+      }
+    }
+  }
+}
+
+// Deterministic single-block reduction of the per-lane statistics.
+__global__ void stats_kernel(DevState st, int64_t B, double* out, int reset) {
+  __shared__ double part[8][256];
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
+    acc[0] += st.st_episodes[b];
+    acc[1] += st.st_wins[b];
+    acc[2] += st.st_fk_ally[b];
+    acc[3] += st.st_ties[b];
+    acc[4] += (double)st.st_len[b];
+    acc[5] += st.st_ret[b];
+    acc[6] += st.st_elims[b];
+    if (reset) {
+      st.st_episodes[b] = st.st_wins[b] = st.st_fk_ally[b] = st.st_ties[b] = st.st_elims[b] = 0;
+      st.st_len[b] = 0;
+      st.st_ret[b] = 0.0;
+    }
+  }
+  for (int k = 0; k < 7; ++k) part[k][threadIdx.x] = acc[k];
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s)
+      for (int k = 0; k < 7; ++k) part[k][threadIdx.x] += part[k][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 7; ++k) out[k] = part[k][0];
+}
+
+__global__ void sincos_debug_kernel(const double* x, double* s, double* c, int64_t n) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    s[k] = libm_sin(x[k]);
+    c[k] = libm_cos(x[k]);
+  }
+}
+
+cudaError_t launch_lanes(const Params& P, int W, int sm_count, cudaStream_t stream,
+                         int* grid_out) {
+  switch (W) {
+    case 1: return launch_lanes_w1(P, sm_count, stream, grid_out);
+    case 2: return launch_lanes_w2(P, sm_count, stream, grid_out);
+    case 4: return launch_lanes_w4(P, sm_count, stream, grid_out);
+    default: return launch_lanes_w8(P, sm_count, stream, grid_out);
+  }
+}
+
+static int grid_for(int64_t n, int threads, int sm_count) {
+  int64_t g = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count * 16;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
+                            int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream) {
+  validate_kernel<<<grid_for(B * N, 256, sm_count), 256, 0, stream>>>(actions, st, cfgs, B, N,
+                                                                      sync);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, int64_t b0, int64_t b1,
+                         int N, int W, int reset_stats, int sm_count, cudaStream_t stream) {
+  int64_t n = b1 - b0;
+  int grid = (int)(n < (int64_t)sm_count * 32 ? n : (int64_t)sm_count * 32);
+  if (grid < 1) return cudaSuccess;
+  spawn_kernel<<<grid, 32 * W, 0, stream>>>(st, cfgs, b0, b1, N, W, reset_stats);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_export(const DevState& st, const tabx_state& d, int64_t B, int N, int W,
+                          int sm_count, cudaStream_t stream) {
+  export_kernel<<<grid_for(B * N, 256, sm_count), 256, 0, stream>>>(st, d, B, N, W);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_import(const DevState& st, const tabx_state& s, int64_t B, int N, int W,
+                          int sm_count, cudaStream_t stream) {
+  import_kernel<<<grid_for(B * N, 256, sm_count), 256, 0, stream>>>(st, s, B, N, W);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats(const DevState& st, int64_t B, double* out, int reset,
+                         cudaStream_t stream) {
+  stats_kernel<<<1, 256, 0, stream>>>(st, B, out, reset);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sincos_debug(const double* x, double* s, double* c, int64_t n,
+                                cudaStream_t stream) {
+  sincos_debug_kernel<<<grid_for(n, 256, 148), 256, 0, stream>>>(x, s, c, n);
+  return cudaGetLastError();
+}
+
+}  // namespace tabx

@@ -1,0 +1,438 @@
+// C ABI (include/tabx.h): handle lifetime, config table, launches.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "tabx_device.cuh"
+
+namespace tabx {
+cudaError_t launch_lanes(const Params& P, int W, int sm_count, cudaStream_t stream, int* grid);
+cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
+                            int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream);
+cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, int64_t b0, int64_t b1,
+                         int N, int W, int reset_stats, int sm_count, cudaStream_t stream);
+cudaError_t launch_export(const DevState& st, const tabx_state& d, int64_t B, int N, int W,
+                          int sm_count, cudaStream_t stream);
+cudaError_t launch_import(const DevState& st, const tabx_state& s, int64_t B, int N, int W,
+                          int sm_count, cudaStream_t stream);
+cudaError_t launch_stats(const DevState& st, int64_t B, double* out, int reset,
+                         cudaStream_t stream);
+cudaError_t launch_sincos_debug(const double* x, double* s, double* c, int64_t n,
+                                cudaStream_t stream);
+}  // namespace tabx
+
+using namespace tabx;
+
+struct tabx_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t B = 0;
+  int N = 0, Z = 0, W = 1, D = 0, G = 0;
+  int auto_reset = 0;
+  int sm_count = 148;
+  bool any_external = false;
+  std::vector<tabx_config> cfg_host;
+  tabx_config* cfg_dev = nullptr;
+  DevState st{};
+  void* arena = nullptr;
+  Sync* sync = nullptr;
+  double* stats_dev = nullptr;
+  const int64_t* last_actions = nullptr;
+};
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+static int cuda_fail(cudaError_t e, const char* what) {
+  g_err = std::string(what) + ": " + cudaGetErrorString(e);
+  return TABX_E_CUDA;
+}
+
+#define TABX_CUDA(call, what)                 \
+  do {                                        \
+    cudaError_t e_ = (call);                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+static int words_for(int N) {
+  int w = (N + 31) / 32;
+  if (w <= 1) return 1;
+  if (w <= 2) return 2;
+  if (w <= 4) return 4;
+  return 8;
+}
+
+static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
+                          const tabx_outputs* out) {
+  Params P;
+  P.st = h->st;
+  P.cfgs = h->cfg_dev;
+  P.sync = h->sync;
+  P.actions = actions;
+  if (out) {
+    P.out = *out;
+  } else {
+    memset(&P.out, 0, sizeof(P.out));
+  }
+  P.B = h->B;
+  P.N = h->N;
+  P.Z = h->Z;
+  P.D = h->D;
+  P.G = h->G;
+  P.auto_reset = h->auto_reset;
+  P.mode = mode;
+  return P;
+}
+
+static int check_outputs(const tabx_outputs* out) {
+  if (!out) return TABX_OK;
+  const float* ptrs[2] = {out->observations, out->final_observations};
+  for (const float* p : ptrs)
+    if (p && (((uintptr_t)p) & 15u)) return fail(TABX_E_ALIGNMENT, "observation buffer must be 16-byte aligned");
+  return TABX_OK;
+}
+
+static int find_or_add_config(tabx_handle* h, const tabx_config* c, int32_t* idx) {
+  if (c->n_units != h->N || c->n_zones != h->Z)
+    return fail(TABX_E_SHAPE, "batched environments must share max_units and max_zones");
+  for (size_t k = 0; k < h->cfg_host.size(); ++k) {
+    if (!memcmp(&h->cfg_host[k], c, sizeof(tabx_config))) {
+      *idx = (int32_t)k;
+      return TABX_OK;
+    }
+  }
+  if (h->cfg_host.size() >= TABX_MAX_CONFIGS)
+    return fail(TABX_E_CAPACITY, "config table full");
+  h->cfg_host.push_back(*c);
+  const size_t k = h->cfg_host.size() - 1;
+  TABX_CUDA(cudaMemcpyAsync(h->cfg_dev + k, c, sizeof(tabx_config), cudaMemcpyHostToDevice,
+                            h->stream),
+            "config upload");
+  if (c->controller[0] == TABX_CTRL_EXTERNAL || c->controller[1] == TABX_CTRL_EXTERNAL)
+    h->any_external = true;
+  *idx = (int32_t)k;
+  return TABX_OK;
+}
+
+extern "C" {
+
+int tabx_abi_version(void) { return TABX_ABI_VERSION; }
+
+const char* tabx_last_error(void) { return g_err.c_str(); }
+
+int32_t tabx_obs_dim(int32_t n, int32_t z) {
+  return TABX_OWN_DIM + (n - 1) * TABX_OTHER_DIM + z * TABX_ZONE_DIM;
+}
+
+int32_t tabx_global_dim(int32_t n, int32_t z) { return n * TABX_OWN_DIM + z * TABX_ZONE_DIM; }
+
+int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* env_config,
+                const uint64_t* seeds, int64_t batch, int32_t auto_reset, int32_t device,
+                void* stream, tabx_handle** out) {
+  if (!configs || n_configs < 1 || !seeds || batch < 1 || !out)
+    return fail(TABX_E_ARGUMENT, "tabx_create: bad argument");
+  const int N = configs[0].n_units, Z = configs[0].n_zones;
+  if (N < 1 || N > TABX_MAX_UNITS || Z < 0 || Z > TABX_MAX_ZONES)
+    return fail(TABX_E_ARGUMENT, "unit / zone capacity out of range");
+  for (int k = 1; k < n_configs; ++k)
+    if (configs[k].n_units != N || configs[k].n_zones != Z)
+      return fail(TABX_E_SHAPE, "batched environments must share max_units and max_zones");
+  if (env_config)
+    for (int64_t b = 0; b < batch; ++b)
+      if (env_config[b] < 0 || env_config[b] >= n_configs)
+        return fail(TABX_E_ARGUMENT, "env_config index out of range");
+  DeviceGuard guard(device);
+  tabx_handle* h = new tabx_handle();
+  h->device = device;
+  h->stream = (cudaStream_t)stream;
+  h->B = batch;
+  h->N = N;
+  h->Z = Z;
+  h->W = words_for(N);
+  h->D = tabx_obs_dim(N, Z);
+  h->G = tabx_global_dim(N, Z);
+  h->auto_reset = auto_reset ? 1 : 0;
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
+
+  const int64_t B = batch, U = batch * N, W = h->W;
+  // arena layout (all sub-arrays 256-byte aligned)
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  size_t o_seed = take(8 * B), o_ep = take(8 * B), o_t = take(4 * B), o_pg = take(8 * B),
+         o_ret = take(8 * B), o_flags = take(B), o_win = take(B), o_rea = take(B),
+         o_fk = take(B), o_cfg = take(4 * B), o_pos = take(16 * U), o_hd = take(8 * U),
+         o_vel = take(16 * U), o_imp = take(16 * U), o_hp = take(8 * U), o_cd = take(8 * U),
+         o_rv = take(8 * U), o_mem = take(16 * U), o_ub = take(U), o_vis = take(4 * U * W),
+         o_atk = take(4 * U * W), o_se = take(4 * B), o_sw = take(4 * B), o_sf = take(4 * B),
+         o_stie = take(4 * B), o_sel = take(4 * B), o_sl = take(8 * B), o_sr = take(8 * B),
+         o_sync = take(sizeof(Sync)), o_stats = take(8 * TABX_NUM_STATS);
+  cudaError_t e = cudaMalloc(&h->arena, off);
+  if (e != cudaSuccess) {
+    delete h;
+    return cuda_fail(e, "state allocation");
+  }
+  e = cudaMalloc((void**)&h->cfg_dev, sizeof(tabx_config) * TABX_MAX_CONFIGS);
+  if (e != cudaSuccess) {
+    cudaFree(h->arena);
+    delete h;
+    return cuda_fail(e, "config table allocation");
+  }
+  char* a = (char*)h->arena;
+  DevState& st = h->st;
+  st.seed = (uint64_t*)(a + o_seed);
+  st.episode = (int64_t*)(a + o_ep);
+  st.t = (int32_t*)(a + o_t);
+  st.prev_gap = (double*)(a + o_pg);
+  st.ep_return = (double*)(a + o_ret);
+  st.flags = (uint8_t*)(a + o_flags);
+  st.winner = (int8_t*)(a + o_win);
+  st.reason = (int8_t*)(a + o_rea);
+  st.first_kill = (int8_t*)(a + o_fk);
+  st.cfg = (int32_t*)(a + o_cfg);
+  st.pos = (double2*)(a + o_pos);
+  st.heading = (double*)(a + o_hd);
+  st.vel = (double2*)(a + o_vel);
+  st.imp_dv = (double2*)(a + o_imp);
+  st.health = (double*)(a + o_hp);
+  st.cooldown = (double*)(a + o_cd);
+  st.reveal = (double*)(a + o_rv);
+  st.mem_pos = (double2*)(a + o_mem);
+  st.ubits = (uint8_t*)(a + o_ub);
+  st.vis = (uint32_t*)(a + o_vis);
+  st.atk = (uint32_t*)(a + o_atk);
+  st.st_episodes = (uint32_t*)(a + o_se);
+  st.st_wins = (uint32_t*)(a + o_sw);
+  st.st_fk_ally = (uint32_t*)(a + o_sf);
+  st.st_ties = (uint32_t*)(a + o_stie);
+  st.st_elims = (uint32_t*)(a + o_sel);
+  st.st_len = (int64_t*)(a + o_sl);
+  st.st_ret = (double*)(a + o_sr);
+  h->sync = (Sync*)(a + o_sync);
+  h->stats_dev = (double*)(a + o_stats);
+
+  int rc = TABX_OK;
+  for (int k = 0; k < n_configs; ++k) {
+    h->cfg_host.push_back(configs[k]);
+    if (configs[k].controller[0] == TABX_CTRL_EXTERNAL ||
+        configs[k].controller[1] == TABX_CTRL_EXTERNAL)
+      h->any_external = true;
+  }
+  e = cudaMemcpyAsync(h->cfg_dev, configs, sizeof(tabx_config) * n_configs,
+                      cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(h->arena, 0, off, h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(st.seed, seeds, 8 * B, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess && env_config)
+    e = cudaMemcpyAsync(st.cfg, env_config, 4 * B, cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(&h->sync->err_index, 0xFF, 8, h->stream);
+  if (e == cudaSuccess) e = launch_spawn(st, h->cfg_dev, 0, B, N, (int)W, 1, h->sm_count, h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // host arrays may be freed
+  if (e != cudaSuccess) {
+    rc = cuda_fail(e, "tabx_create");
+    cudaFree(h->cfg_dev);
+    cudaFree(h->arena);
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return TABX_OK;
+}
+
+int tabx_destroy(tabx_handle* h) {
+  if (!h) return TABX_OK;
+  DeviceGuard guard(h->device);
+  cudaStreamSynchronize(h->stream);
+  cudaFree(h->cfg_dev);
+  cudaFree(h->arena);
+  delete h;
+  return TABX_OK;
+}
+
+int tabx_set_stream(tabx_handle* h, void* stream) {
+  if (!h) return fail(TABX_E_ARGUMENT, "null handle");
+  h->stream = (cudaStream_t)stream;
+  return TABX_OK;
+}
+
+int tabx_dims(const tabx_handle* h, int64_t* batch, int32_t* n_units, int32_t* n_zones,
+              int32_t* obs_dim, int32_t* global_dim) {
+  if (!h) return fail(TABX_E_ARGUMENT, "null handle");
+  if (batch) *batch = h->B;
+  if (n_units) *n_units = h->N;
+  if (n_zones) *n_zones = h->Z;
+  if (obs_dim) *obs_dim = h->D;
+  if (global_dim) *global_dim = h->G;
+  return TABX_OK;
+}
+
+int tabx_init_output(tabx_handle* h, const tabx_outputs* out) {
+  if (!h) return fail(TABX_E_ARGUMENT, "null handle");
+  int rc = check_outputs(out);
+  if (rc) return rc;
+  DeviceGuard guard(h->device);
+  Params P = make_params(h, MODE_INIT, nullptr, out);
+  TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "init_output launch");
+  // fresh caches everywhere: nothing left to refresh
+  TABX_CUDA(cudaMemsetAsync(h->sync->refresh, 0, sizeof(h->sync->refresh), h->stream),
+            "refresh clear");
+  return TABX_OK;
+}
+
+int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
+  if (!h) return fail(TABX_E_ARGUMENT, "null handle");
+  int rc = check_outputs(out);
+  if (rc) return rc;
+  DeviceGuard guard(h->device);
+  if (actions && h->any_external) {
+    TABX_CUDA(launch_validate(actions, h->st, h->cfg_dev, h->B, h->N, h->sync, h->sm_count,
+                              h->stream),
+              "validate launch");
+  }
+  h->last_actions = actions;
+  Params P = make_params(h, MODE_STEP, actions, out);
+  TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "step launch");
+  return TABX_OK;
+}
+
+int tabx_reset_env(tabx_handle* h, int64_t b, const tabx_config* config, uint64_t seed,
+                   int32_t has_seed, const tabx_outputs* out) {
+  if (!h || b < 0 || b >= h->B) return fail(TABX_E_ARGUMENT, "tabx_reset_env: bad lane");
+  int rc = check_outputs(out);
+  if (rc) return rc;
+  DeviceGuard guard(h->device);
+  if (config) {
+    int32_t idx;
+    rc = find_or_add_config(h, config, &idx);
+    if (rc) return rc;
+    TABX_CUDA(cudaMemcpyAsync(h->st.cfg + b, &idx, 4, cudaMemcpyHostToDevice, h->stream),
+              "config index");
+    TABX_CUDA(cudaStreamSynchronize(h->stream), "reset_env sync");
+  }
+  if (has_seed) {
+    TABX_CUDA(cudaMemcpyAsync(h->st.seed + b, &seed, 8, cudaMemcpyHostToDevice, h->stream),
+              "seed upload");
+    TABX_CUDA(cudaStreamSynchronize(h->stream), "reset_env sync");
+  }
+  TABX_CUDA(launch_spawn(h->st, h->cfg_dev, b, b + 1, h->N, h->W, 0, h->sm_count, h->stream),
+            "spawn launch");
+  return tabx_init_output(h, out);
+}
+
+int tabx_respawn_all(tabx_handle* h, const uint64_t* seeds, const int32_t* env_config) {
+  if (!h || !seeds) return fail(TABX_E_ARGUMENT, "tabx_respawn_all: bad argument");
+  DeviceGuard guard(h->device);
+  if (env_config)
+    for (int64_t b = 0; b < h->B; ++b)
+      if (env_config[b] < 0 || env_config[b] >= (int32_t)h->cfg_host.size())
+        return fail(TABX_E_ARGUMENT, "env_config index out of range");
+  TABX_CUDA(cudaMemcpyAsync(h->st.seed, seeds, 8 * h->B, cudaMemcpyHostToDevice, h->stream),
+            "seeds");
+  TABX_CUDA(cudaMemsetAsync(h->st.episode, 0, 8 * h->B, h->stream), "episodes");
+  if (env_config) {
+    TABX_CUDA(cudaMemcpyAsync(h->st.cfg, env_config, 4 * h->B, cudaMemcpyHostToDevice, h->stream),
+              "env config");
+  } else {
+    TABX_CUDA(cudaMemsetAsync(h->st.cfg, 0, 4 * h->B, h->stream), "env config");
+  }
+  TABX_CUDA(cudaMemsetAsync(&h->sync->err_index, 0xFF, 8, h->stream), "error clear");
+  TABX_CUDA(launch_spawn(h->st, h->cfg_dev, 0, h->B, h->N, h->W, 1, h->sm_count, h->stream),
+            "spawn launch");
+  TABX_CUDA(cudaStreamSynchronize(h->stream), "respawn sync");
+  return TABX_OK;
+}
+
+int tabx_export_state(tabx_handle* h, const tabx_state* dst) {
+  if (!h || !dst) return fail(TABX_E_ARGUMENT, "tabx_export_state: bad argument");
+  DeviceGuard guard(h->device);
+  // caches pending a batch refresh are materialised first (refresh_caches)
+  Params P = make_params(h, MODE_REFRESH, nullptr, nullptr);
+  TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "refresh launch");
+  TABX_CUDA(launch_export(h->st, *dst, h->B, h->N, h->W, h->sm_count, h->stream), "export");
+  return TABX_OK;
+}
+
+int tabx_import_state(tabx_handle* h, const tabx_state* src) {
+  if (!h || !src) return fail(TABX_E_ARGUMENT, "tabx_import_state: bad argument");
+  DeviceGuard guard(h->device);
+  TABX_CUDA(launch_import(h->st, *src, h->B, h->N, h->W, h->sm_count, h->stream), "import");
+  TABX_CUDA(cudaMemsetAsync(h->sync->refresh, 0, sizeof(h->sync->refresh), h->stream),
+            "refresh clear");
+  return TABX_OK;
+}
+
+int tabx_get_error(tabx_handle* h, tabx_error* err, int32_t clear) {
+  if (!h || !err) return fail(TABX_E_ARGUMENT, "tabx_get_error: bad argument");
+  DeviceGuard guard(h->device);
+  unsigned long long idx = NO_ERROR;
+  TABX_CUDA(cudaMemcpyAsync(&idx, &h->sync->err_index, 8, cudaMemcpyDeviceToHost, h->stream),
+            "error read");
+  TABX_CUDA(cudaStreamSynchronize(h->stream), "error sync");
+  memset(err, 0, sizeof(*err));
+  if (idx != NO_ERROR) {
+    err->code = TABX_E_ACTION_MASK;
+    err->env = (int64_t)(idx / (unsigned long long)h->N);
+    err->unit = (int32_t)(idx % (unsigned long long)h->N);
+    int64_t a = 0;
+    if (h->last_actions) {
+      TABX_CUDA(cudaMemcpy(&a, h->last_actions + idx, 8, cudaMemcpyDeviceToHost), "action read");
+    }
+    err->action = a;
+    if (clear) {
+      TABX_CUDA(cudaMemsetAsync(&h->sync->err_index, 0xFF, 8, h->stream), "error clear");
+      TABX_CUDA(cudaStreamSynchronize(h->stream), "error clear sync");
+    }
+  }
+  return TABX_OK;
+}
+
+int tabx_episode_stats(tabx_handle* h, double* dst_host, double* dst_device, int32_t reset) {
+  if (!h) return fail(TABX_E_ARGUMENT, "null handle");
+  DeviceGuard guard(h->device);
+  double* out = dst_device ? dst_device : h->stats_dev;
+  TABX_CUDA(cudaMemsetAsync(out, 0, 8 * TABX_NUM_STATS, h->stream), "stats clear");
+  TABX_CUDA(launch_stats(h->st, h->B, out, reset, h->stream), "stats launch");
+  if (dst_host) {
+    TABX_CUDA(cudaMemcpyAsync(dst_host, out, 8 * TABX_NUM_STATS, cudaMemcpyDeviceToHost,
+                              h->stream),
+              "stats read");
+    TABX_CUDA(cudaStreamSynchronize(h->stream), "stats sync");
+  }
+  return TABX_OK;
+}
+
+int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state) {
+  if (config) *config = (int64_t)sizeof(tabx_config);
+  if (outputs) *outputs = (int64_t)sizeof(tabx_outputs);
+  if (state) *state = (int64_t)sizeof(tabx_state);
+  return TABX_OK;
+}
+
+int tabx_debug_sincos(const double* x, double* s, double* c, int64_t n, void* stream) {
+  TABX_CUDA(launch_sincos_debug(x, s, c, n, (cudaStream_t)stream), "sincos launch");
+  return TABX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,1104 @@
+// The batched environment step on sm_100a.
+//
+// One environment per "env group" of NT = 32*W threads, thread i = unit i
+// (N <= NT).  W = 1 (N <= 32) packs EPB environments per CTA, one per warp,
+// synchronised with __syncwarp only; W > 1 runs one environment per CTA.
+// A persistent grid-stride loop walks the lanes.  Unit state lives in
+// registers, the cross-unit views (positions, headings, flags, cache rows)
+// in shared memory; the O(N^2) pair passes are row-owned (thread i scans
+// j = 0..N-1) with the visibility / attackable rows built as N-bit masks.
+// Order-dependent reductions (Gauss-Seidel contacts, numpy's pairwise team
+// sums) run on one thread over shared memory, exactly in reference order.
+// The observation block of each environment is generated column-by-column
+// from shared memory and streamed out with 16-byte stores.
+//
+// Every stage cites the reference line it restates; arithmetic is float64,
+// compiled with -fmad=false so no product is fused that numpy rounds.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tabx_device.cuh"
+#include "tabx_math.cuh"
+
+namespace tabx {
+
+// ------------------------------------------------------------------ rng --
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// rng.py:31-37
+__device__ __forceinline__ uint64_t key_hash(uint64_t seed, uint64_t step, uint64_t tag,
+                                             uint64_t lane) {
+  uint64_t h = mix64(seed + 0x9E3779B97F4A7C15ull * tag);
+  h = mix64(h + step * 0xC2B2AE3D27D4EB4Full);
+  return mix64(h + lane * 0x165667B19E3779F9ull);
+}
+
+// rng.py:40-43
+__device__ __forceinline__ double uniform53(uint64_t seed, uint64_t step, uint64_t tag,
+                                            uint64_t lane) {
+  return (double)(key_hash(seed, step, tag, lane) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+// ------------------------------------------------------------- helpers --
+constexpr uint32_t UF_ACTIVE = 1, UF_ALIVE = 2, UF_ENEMY = 4, UF_KIN = 8, UF_INJURED = 16;
+
+template <int W>
+struct EnvSmem {
+  static constexpr int NT = 32 * W;
+  double px[NT], py[NT], ch[NT], sh[NT], rad[NT], mh[NT], rv[NT], dmg[NT];
+  double vx[NT], vy[NT], sx[NT], sy[NT];
+  float own[NT][TABX_OWN_DIM];
+  uint32_t vis[NT * W], atk[NT * W], touch[NT * W];
+  uint32_t uf[NT];
+  uint32_t zin[NT];
+  int32_t tgt[NT];
+  uint32_t ball[W];
+  double red[2];
+};
+
+template <int W>
+__device__ __forceinline__ void env_sync() {
+  if (W == 1) {
+    __syncwarp();
+  } else {
+    __syncthreads();
+  }
+}
+
+// Env-wide ballot: word k holds predicates of units 32k..32k+31.
+template <int W>
+__device__ __forceinline__ void env_ballot(bool p, EnvSmem<W>& S, int i, uint32_t (&m)[W]) {
+  uint32_t b = __ballot_sync(0xffffffffu, p);
+  if (W == 1) {
+    m[0] = b;
+  } else {
+    if ((i & 31) == 0) S.ball[i >> 5] = b;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < W; ++k) m[k] = S.ball[k];
+    __syncthreads();
+  }
+}
+
+template <int W>
+__device__ __forceinline__ bool env_any(bool p, EnvSmem<W>& S, int i) {
+  uint32_t m[W];
+  env_ballot<W>(p, S, i, m);
+  uint32_t a = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) a |= m[k];
+  return a != 0;
+}
+
+template <int W>
+__device__ __forceinline__ int env_count(bool p, EnvSmem<W>& S, int i) {
+  uint32_t m[W];
+  env_ballot<W>(p, S, i, m);
+  int c = 0;
+#pragma unroll
+  for (int k = 0; k < W; ++k) c += __popc(m[k]);
+  return c;
+}
+
+__device__ __forceinline__ bool bit_of(const uint32_t* row, int j) {
+  return (row[j >> 5] >> (j & 31)) & 1u;
+}
+
+// Zone membership bits at (x, y) (arrays.py:329-335).
+__device__ __forceinline__ uint32_t zone_bits(const tabx_config* __restrict__ C, int Z, double x,
+                                              double y) {
+  uint32_t bits = 0;
+  for (int z = 0; z < Z; ++z) {
+    if (C->zone_type[z] == TABX_ZONE_NONE) continue;
+    double qx = (x - C->zone_cx[z]) / C->zone_ax[z];
+    double qy = (y - C->zone_cy[z]) / C->zone_ay[z];
+    if (qx * qx + qy * qy <= 1.0) bits |= 1u << z;
+  }
+  return bits;
+}
+
+__device__ __forceinline__ uint32_t zone_type_mask(const tabx_config* __restrict__ C, int Z,
+                                                   int type) {
+  uint32_t m = 0;
+  for (int z = 0; z < Z; ++z)
+    if (C->zone_type[z] == type) m |= 1u << z;
+  return m;
+}
+
+// effective_speed multiplier: sequential product over zones (arrays.py:338-343)
+__device__ __forceinline__ double swamp_mult(const tabx_config* __restrict__ C, int Z,
+                                             uint32_t zin, uint32_t swamp_m) {
+  double m = 1.0;
+  uint32_t hit = zin & swamp_m;
+  for (int z = 0; z < Z; ++z) m = m * (((hit >> z) & 1u) ? C->zone_effect[z] : 1.0);
+  return m;
+}
+
+// lava burn rate: numpy last-axis sum over Z (environment.py:273)
+__device__ __forceinline__ double lava_sum(const tabx_config* __restrict__ C, int Z, uint32_t zin,
+                                           uint32_t lava_m) {
+  uint32_t hit = zin & lava_m;
+  if (Z < 8) {
+    double r = 0.0;
+    for (int z = 0; z < Z; ++z)
+      if ((hit >> z) & 1u) r += C->zone_effect[z];
+    return r;
+  }
+  double v[TABX_MAX_ZONES];
+  for (int z = 0; z < Z; ++z) v[z] = ((hit >> z) & 1u) ? C->zone_effect[z] : 0.0;
+  return pairwise_sum(v, Z);
+}
+
+// Index of the floor(u*n)-th legal action (environment.py:198-201).
+__device__ __forceinline__ int kth_legal(uint32_t mask7, double u) {
+  int n = __popc(mask7);
+  long long k = (long long)(u * (double)n);
+  if (k > n - 1) k = n - 1;
+  uint32_t m = mask7;
+  for (long long s = 0; s < k; ++s) m &= m - 1;
+  return __ffs(m) - 1;
+}
+
+// Move choice: argmin / argmax of squared distance over the 4 axis moves
+// (heuristics.py:75-84); ties go to the lowest action id.
+__device__ __forceinline__ int best_move(double px, double py, double gx, double gy, double step,
+                                         bool away) {
+  const double dxs[4] = {0.0, 0.0, 1.0, -1.0};
+  const double dys[4] = {1.0, -1.0, 0.0, 0.0};
+  int best = 0;
+  double bv = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double cx = px + dxs[k] * step;
+    double cy = py + dys[k] * step;
+    double ex = cx - gx, ey = cy - gy;
+    double v = ex * ex + ey * ey;
+    if (k == 0 || (away ? (v > bv) : (v < bv))) {
+      bv = v;
+      best = k;
+    }
+  }
+  return best;
+}
+
+struct UnitStatic {
+  double rad, mh, mass, inv_mass, speed, dmg, range, ucd, sangle, cos_half, srange;
+  bool active, enemy, kin, assassin, ranger, healer;
+};
+
+__device__ __forceinline__ UnitStatic load_static(const tabx_config* __restrict__ C, int i,
+                                                  bool valid) {
+  UnitStatic u;
+  if (valid) {
+    u.rad = C->radius[i];
+    u.mh = C->max_health[i];
+    u.mass = C->mass[i];
+    u.inv_mass = C->inv_mass[i];
+    u.speed = C->speed[i];
+    u.dmg = C->damage[i];
+    u.range = C->attack_range[i];
+    u.ucd = C->cooldown[i];
+    u.sangle = C->sight_angle[i];
+    u.cos_half = C->sight_cos_half[i];
+    u.srange = C->sight_range[i];
+    u.active = C->active[i] != 0;
+    u.enemy = C->team[i] != 0;
+    u.kin = C->kinematic[i] != 0;
+    u.assassin = C->role_assassin[i] != 0;
+    u.ranger = C->role_ranger[i] != 0;
+    u.healer = C->role_healer[i] != 0;
+  } else {
+    u.rad = 0.0;
+    u.mh = 1.0;
+    u.mass = 1.0;
+    u.inv_mass = 1.0;
+    u.speed = u.dmg = u.range = u.ucd = u.sangle = u.srange = 0.0;
+    u.cos_half = 1.0;
+    u.active = u.enemy = u.kin = u.assassin = u.ranger = u.healer = false;
+  }
+  return u;
+}
+
+// Visibility / attackable rows of observer i and its nearest attackable
+// target (perception.py:52-96, combat.py:16-83).  Reads positions, headings,
+// reveal timers, flags and zone bits of every unit from shared memory.
+template <int W>
+__device__ __forceinline__ void cache_row(const EnvSmem<W>& S, int i, int N, const UnitStatic& U,
+                                          uint32_t uf_i, uint32_t bush_m, uint32_t (&vis)[W],
+                                          uint32_t (&atk)[W], int& tgt) {
+#pragma unroll
+  for (int k = 0; k < W; ++k) vis[k] = atk[k] = 0u;
+  tgt = -1;
+  const double px = S.px[i], py = S.py[i], ch = S.ch[i], sh = S.sh[i];
+  const bool act_i = (uf_i & UF_ACTIVE) != 0;
+  const bool live_i = act_i && (uf_i & UF_ALIVE);
+  const bool enemy_i = (uf_i & UF_ENEMY) != 0;
+  const uint32_t bush_i = S.zin[i] & bush_m;
+  double best = 0.0;
+  if (!act_i) return;  // vis requires both active; atk requires vis
+  for (int j = 0; j < N; ++j) {
+    const uint32_t uj = S.uf[j];
+    if (!(uj & UF_ACTIVE)) continue;
+    const double dx = S.px[j] - px;
+    const double dy = S.py[j] - py;
+    const double dist = sqrt(dx * dx + dy * dy);
+    const double lx = dx * ch + dy * sh;
+    const double cdev = dist > 0.0 ? lx / dist : 1.0;
+    const bool wedge = cdev >= U.cos_half;
+    if (!(dist <= U.srange && wedge)) continue;
+    const bool foe = ((uj & UF_ENEMY) != 0) != enemy_i;
+    const uint32_t bush_j = S.zin[j] & bush_m;
+    const bool hidden = bush_j != 0u && foe && (bush_i & bush_j) == 0u && S.rv[j] <= 0.0;
+    if (hidden) continue;
+    vis[j >> 5] |= 1u << (j & 31);
+    const bool role = U.dmg > 0.0 ? foe : (U.dmg < 0.0 && !foe);
+    if (!(role && live_i && (uj & UF_ALIVE) && j != i)) continue;
+    const double ly = (-dx) * sh + dy * ch;
+    const double cx = np_clip(lx, 0.0, U.range);
+    const double cy = np_clip(ly, -U.rad, U.rad);
+    const double gx = lx - cx, gy = ly - cy;
+    const double rj = S.rad[j];
+    if (gx * gx + gy * gy <= rj * rj) {
+      atk[j >> 5] |= 1u << (j & 31);
+      if (tgt < 0 || dist < best) {
+        best = dist;
+        tgt = j;
+      }
+    }
+  }
+}
+
+// Column descriptors of one observation row: kind<<13 | payload.
+//  kind 0: own feature f;  kind 1: other block k (j = k or k+1), feature f
+//  (payload k<<5 | f);  kind 2: zone z feature f (payload z<<3 | f).
+__device__ __forceinline__ uint16_t column_desc(int c, int N) {
+  if (c < TABX_OWN_DIM) return (uint16_t)c;
+  int o = c - TABX_OWN_DIM;
+  if (o < (N - 1) * TABX_OTHER_DIM) {
+    int k = o / TABX_OTHER_DIM, f = o - k * TABX_OTHER_DIM;
+    return (uint16_t)((1 << 13) | (k << 5) | f);
+  }
+  o -= (N - 1) * TABX_OTHER_DIM;
+  int z = o / TABX_ZONE_DIM, f = o - z * TABX_ZONE_DIM;
+  return (uint16_t)((2 << 13) | (z << 3) | f);
+}
+
+// One observation element (perception.py:159-192).
+template <int W>
+__device__ __forceinline__ float obs_value(const EnvSmem<W>& S, const uint16_t* __restrict__ tab,
+                                           const tabx_config* __restrict__ C, int i, int c,
+                                           double fw, double fh) {
+  if (!(S.uf[i] & UF_ACTIVE)) return 0.0f;
+  const uint32_t d = tab[c];
+  const uint32_t kind = d >> 13;
+  if (kind == 0) return S.own[i][d];
+  if (kind == 1) {
+    const int k = (d >> 5) & 255, f = d & 31;
+    const int j = k + (k >= i ? 1 : 0);
+    if (!(bit_of(&S.vis[i * W], j) && (S.uf[j] & UF_ACTIVE))) return 0.0f;
+    if (f == 2) return __double2float_rn((S.px[j] - S.px[i]) / fw);
+    if (f == 3) return __double2float_rn((S.py[j] - S.py[i]) / fh);
+    if (f == 15) return (S.uf[j] & UF_ENEMY) ? 1.0f : 0.0f;
+    if (f == 16) return bit_of(&S.atk[i * W], j) ? 1.0f : 0.0f;
+    return S.own[j][f];
+  }
+  const int z = (d >> 3) & 31, f = d & 7;
+  const int ty = C->zone_type[z];
+  if (ty == TABX_ZONE_NONE) return 0.0f;
+  switch (f) {
+    case 0: case 1: case 2: return ty == f + 1 ? 1.0f : 0.0f;
+    case 3: return __double2float_rn((C->zone_cx[z] - S.px[i]) / fw);
+    case 4: return __double2float_rn((C->zone_cy[z] - S.py[i]) / fh);
+    case 5: return __double2float_rn(C->zone_ax[z]);
+    case 6: return __double2float_rn(C->zone_ay[z]);
+    default: return __double2float_rn(C->zone_effect[z]);
+  }
+}
+
+// Stream the env's [N, D] observation block (flat, 16-byte stores in the
+// aligned body, scalar head/tail when N*D is not a multiple of 4).
+template <int W>
+__device__ __forceinline__ void write_obs(float* __restrict__ dst, int64_t b, int N, int D,
+                                          const EnvSmem<W>& S, const uint16_t* __restrict__ tab,
+                                          const tabx_config* __restrict__ C, int tid) {
+  constexpr int NT = 32 * W;
+  const int64_t E = (int64_t)N * D;
+  const int64_t start = b * E;
+  const double fw = C->field_w, fh = C->field_h;
+  int head = (int)((4 - (start & 3)) & 3);
+  if (head > E) head = (int)E;
+  for (int e = tid; e < head; e += NT) {
+    int i = e / D, c = e - i * D;
+    dst[start + e] = obs_value<W>(S, tab, C, i, c, fw, fh);
+  }
+  const int64_t nvec = (E - head) >> 2;
+  float4* __restrict__ v4 = reinterpret_cast<float4*>(dst + start + head);
+  for (int64_t q = tid; q < nvec; q += NT) {
+    int e0 = head + (int)(q << 2);
+    int i = e0 / D, c = e0 - i * D;
+    float r[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      r[k] = obs_value<W>(S, tab, C, i, c, fw, fh);
+      if (++c == D) {
+        c = 0;
+        ++i;
+      }
+    }
+    __stcs(v4 + q, make_float4(r[0], r[1], r[2], r[3]));
+  }
+  for (int64_t e = head + (nvec << 2) + tid; e < E; e += NT) {
+    int i = (int)(e / D), c = (int)(e - (int64_t)i * D);
+    dst[start + e] = obs_value<W>(S, tab, C, i, c, fw, fh);
+  }
+}
+
+// Global state row (perception.py:194-200): own blocks then absolute zones.
+template <int W>
+__device__ __forceinline__ void write_global(float* __restrict__ dst, int64_t b, int N, int Z,
+                                             int G, const EnvSmem<W>& S,
+                                             const tabx_config* __restrict__ C, int tid) {
+  constexpr int NT = 32 * W;
+  float* row = dst + b * (int64_t)G;
+  const int own_cols = N * TABX_OWN_DIM;
+  for (int c = tid; c < G; c += NT) {
+    float v;
+    if (c < own_cols) {
+      int i = c / TABX_OWN_DIM, f = c - i * TABX_OWN_DIM;
+      v = S.own[i][f];
+    } else {
+      int o = c - own_cols;
+      int z = o >> 3, f = o & 7;
+      int ty = C->zone_type[z];
+      if (ty == TABX_ZONE_NONE) {
+        v = 0.0f;
+      } else {
+        switch (f) {
+          case 0: case 1: case 2: v = ty == f + 1 ? 1.0f : 0.0f; break;
+          case 3: v = __double2float_rn(C->zone_cx[z] / C->field_w); break;
+          case 4: v = __double2float_rn(C->zone_cy[z] / C->field_h); break;
+          case 5: v = __double2float_rn(C->zone_ax[z]); break;
+          case 6: v = __double2float_rn(C->zone_ay[z]); break;
+          default: v = __double2float_rn(C->zone_effect[z]); break;
+        }
+      }
+    }
+    row[c] = v;
+  }
+}
+
+// Own-feature block of unit i (perception.py:108-132) rounded to float32.
+__device__ __forceinline__ void own_features(float* o, const UnitStatic& U, double hp, double px,
+                                             double py, double ch, double sh, double cd,
+                                             bool alive, double fw, double fh) {
+  if (!U.active) {
+#pragma unroll
+    for (int f = 0; f < TABX_OWN_DIM; ++f) o[f] = 0.0f;
+    return;
+  }
+  o[0] = __double2float_rn(hp / U.mh);
+  o[1] = __double2float_rn(U.mh / 1000.0);
+  o[2] = __double2float_rn(px / fw);
+  o[3] = __double2float_rn(py / fh);
+  o[4] = __double2float_rn(ch);
+  o[5] = __double2float_rn(sh);
+  o[6] = __double2float_rn(U.range);
+  o[7] = __double2float_rn(U.dmg);
+  o[8] = __double2float_rn(cd);
+  o[9] = U.ucd > 0.0 ? __double2float_rn(cd / U.ucd) : 0.0f;
+  o[10] = __double2float_rn(U.rad);
+  o[11] = __double2float_rn(U.mass);
+  o[12] = __double2float_rn(U.sangle);
+  o[13] = alive ? 1.0f : 0.0f;
+  o[14] = __double2float_rn(U.speed);
+}
+
+// Team health ratio sums in numpy pairwise order (arrays.py:390-400); one
+// thread, values staged in S.vx (ally) / S.vy (enemy).
+template <int W>
+__device__ __forceinline__ void team_ratios(EnvSmem<W>& S, int i, int N, bool active, bool enemy,
+                                            double hp, double mh, int n_ally, int n_enemy,
+                                            double& ra, double& re) {
+  S.vx[i] = (active && !enemy) ? hp / mh : 0.0;
+  S.vy[i] = (active && enemy) ? hp / mh : 0.0;
+  env_sync<W>();
+  if (i == 0) {
+    double ca = (double)(n_ally > 1 ? n_ally : 1);
+    double ce = (double)(n_enemy > 1 ? n_enemy : 1);
+    S.red[0] = pairwise_sum(S.vx, N) / ca;
+    S.red[1] = pairwise_sum(S.vy, N) / ce;
+  }
+  env_sync<W>();
+  ra = S.red[0];
+  re = S.red[1];
+  env_sync<W>();
+}
+
+// Heuristic opponent decision for unit i (heuristics.py:103-243).
+// Returns the action and updates the scripted-controller memory.
+template <int W>
+__device__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
+                               int N, int Z, const UnitStatic& U, const uint32_t (&vis)[W],
+                               const uint32_t (&atk)[W], double hd, double cd, double step,
+                               uint32_t mask7, double u_explore, double u_pick, double eps,
+                               double xi, uint32_t bush_m, double& mx, double& my, bool& memv) {
+  const double px = S.px[i], py = S.py[i];
+  // target candidates: visible, alive & active, not self
+  double bf = 0.0, bi = 0.0, bn = 0.0, bm = 0.0, bmd = 0.0;
+  int tf = -1, ti = -1, tn = -1, tm = -1;
+  for (int j = 0; j < N; ++j) {
+    const uint32_t uj = S.uf[j];
+    if (j == i || !bit_of(vis, j) || (uj & (UF_ACTIVE | UF_ALIVE)) != (UF_ACTIVE | UF_ALIVE))
+      continue;
+    const double dx = S.px[j] - px, dy = S.py[j] - py;
+    const double d = sqrt(dx * dx + dy * dy);
+    const bool foe = ((uj & UF_ENEMY) != 0) != U.enemy;
+    if (!foe) {
+      if (tf < 0 || d < bf) { bf = d; tf = j; }
+      if ((uj & UF_INJURED) && (ti < 0 || d < bi)) { bi = d; ti = j; }
+    } else {
+      if (tn < 0 || d < bn) { bn = d; tn = j; }
+      const double m = S.mh[j];
+      if (tm < 0 || m < bm || (m == bm && d < bmd)) { bm = m; bmd = d; tm = j; }
+    }
+  }
+  int tgt;
+  bool has;
+  if (U.healer) {
+    has = tf >= 0;
+    tgt = ti >= 0 ? ti : (tf >= 0 ? tf : 0);
+  } else if (U.assassin) {
+    has = tm >= 0;
+    tgt = tm >= 0 ? tm : 0;
+  } else {
+    has = tn >= 0;
+    tgt = tn >= 0 ? tn : 0;
+  }
+  const bool has_near = tn >= 0;
+  const double tpx = S.px[tgt], tpy = S.py[tgt], tr = S.rad[tgt];
+
+  // memory validity (heuristics.py:208-209), needed for the update either way
+  const double gx = px - mx, gy = py - my;
+  const bool mem_ok = memv && (sqrt(gx * gx + gy * gy) > U.rad);
+
+  int act = -1;
+  if (has && bit_of(atk, tgt) && cd <= 0.0) act = A_ATTACK;
+  if (act < 0 && has) {
+    // _aligned_after_rotate (heuristics.py:87-100): heading + rot_step unwrapped
+    const double h2 = hd + C->rot_step;
+    const double c2 = libm_cos(h2), s2 = libm_sin(h2);
+    const double dx = tpx - px, dy = tpy - py;
+    const double lx = dx * c2 + dy * s2;
+    const double ly = (-dx) * s2 + dy * c2;
+    const double cx = np_clip(lx, 0.0, U.range);
+    const double cy = np_clip(ly, -U.rad, U.rad);
+    const double ex = lx - cx, ey = ly - cy;
+    const bool box = ex * ex + ey * ey <= tr * tr;
+    const double dist = sqrt(dx * dx + dy * dy);
+    const double cdev = dist > 0.0 ? lx / dist : 1.0;
+    if (box && cdev >= U.cos_half) act = A_ROTATE;
+  }
+  if (act < 0 && U.ranger && has_near && bn < xi * U.range)
+    act = best_move(px, py, S.px[tn], S.py[tn], step, true);
+  if (act < 0 && has) {
+    const double touch = U.rad + tr + 0.5;
+    double gxd, gyd;
+    if (U.healer) {
+      gxd = tpx;
+      gyd = tpy;
+    } else if (U.assassin) {
+      gxd = tpx - S.ch[tgt] * touch;
+      gyd = tpy - S.sh[tgt] * touch;
+    } else {
+      const double standoff = np_max(0.8 * U.range, touch);
+      gxd = tpx + S.ch[tgt] * standoff;
+      gyd = tpy + S.sh[tgt] * standoff;
+    }
+    act = best_move(px, py, gxd, gyd, step, false);
+  }
+  if (act < 0 && mem_ok) act = best_move(px, py, mx, my, step, false);
+  if (act < 0 && Z > 0 && U.ranger && bush_m != 0u && (S.zin[i] & bush_m) == 0u) {
+    int nb = -1;
+    double bd = 0.0;
+    for (int z = 0; z < Z; ++z) {
+      if (!((bush_m >> z) & 1u)) continue;
+      const double ex = C->zone_cx[z] - px, ey = C->zone_cy[z] - py;
+      const double d = sqrt(ex * ex + ey * ey);
+      if (nb < 0 || d < bd) { bd = d; nb = z; }
+    }
+    act = best_move(px, py, C->zone_cx[nb], C->zone_cy[nb], step, false);
+  }
+  if (act < 0) act = A_ROTATE;
+  if (u_explore < eps) act = kth_legal(mask7, u_pick);
+  if (has) {
+    mx = tpx;
+    my = tpy;
+  }
+  memv = has || mem_ok;
+  return act;
+}
+
+// ---------------------------------------------------------------- lane ---
+template <int W>
+__device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
+                         const uint16_t* __restrict__ tab, bool refresh, uint32_t step_no) {
+  const int N = P.N, Z = P.Z;
+  const bool valid = i < N;
+  const int64_t u = b * N + i;
+  const DevState& st = P.st;
+  const tabx_config* __restrict__ C = P.cfgs + st.cfg[b];
+  const UnitStatic U = load_static(C, i, valid);
+  const uint32_t bush_m = zone_type_mask(C, Z, TABX_ZONE_BUSH);
+  const uint32_t lava_m = zone_type_mask(C, Z, TABX_ZONE_LAVA);
+  const uint32_t swamp_m = zone_type_mask(C, Z, TABX_ZONE_SWAMP);
+  const double dt = C->dt, fw = C->field_w, fh = C->field_h;
+
+  // ---- lane + unit state
+  uint8_t lf = st.flags[b];
+  const bool running = !(lf & F_DONE);
+  int32_t t = st.t[b];
+  uint64_t seed = st.seed[b];
+  double prev_gap = st.prev_gap[b];
+  double ep_ret = st.ep_return[b];
+  int winner = st.winner[b], reason = st.reason[b], fk = st.first_kill[b];
+
+  double px = 0.0, py = 0.0, hd = 0.0, hp = 0.0, cd = 0.0, rv = 0.0;
+  double ivx = 0.0, ivy = 0.0, vlx = 0.0, vly = 0.0, mx = 0.0, my = 0.0;
+  bool alive = false, memv = false;
+  if (valid) {
+    const double2 p = st.pos[u];
+    px = p.x;
+    py = p.y;
+    hd = st.heading[u];
+    hp = st.health[u];
+    cd = st.cooldown[u];
+    rv = st.reveal[u];
+    const double2 iv = st.imp_dv[u];
+    ivx = iv.x;
+    ivy = iv.y;
+    const double2 vv = st.vel[u];
+    vlx = vv.x;
+    vly = vv.y;
+    const double2 m = st.mem_pos[u];
+    mx = m.x;
+    my = m.y;
+    const uint8_t ub = st.ubits[u];
+    alive = ub & U_ALIVE;
+    memv = ub & U_MEMV;
+  }
+  double ch = libm_cos(hd), sh = libm_sin(hd);
+
+  auto publish = [&](void) {
+    S.px[i] = px;
+    S.py[i] = py;
+    S.ch[i] = ch;
+    S.sh[i] = sh;
+    S.rad[i] = U.rad;
+    S.mh[i] = U.mh;
+    S.rv[i] = rv;
+    S.dmg[i] = U.dmg;
+    S.uf[i] = (U.active ? UF_ACTIVE : 0u) | (alive ? UF_ALIVE : 0u) | (U.enemy ? UF_ENEMY : 0u) |
+              (U.kin ? UF_KIN : 0u) | (hp < U.mh ? UF_INJURED : 0u);
+    S.zin[i] = valid ? zone_bits(C, Z, px, py) : 0u;
+  };
+
+  const int n_ally = env_count<W>(valid && U.active && !U.enemy, S, i);
+  const int n_enemy = env_count<W>(valid && U.active && U.enemy, S, i);
+
+  uint32_t vis[W], atk[W];
+  int tgt = -1;
+
+  if (P.mode != MODE_STEP) {
+    // init_output / refresh_caches (environment.py:147-151, :351-374)
+    publish();
+    env_sync<W>();
+    if (P.mode == MODE_REFRESH) {
+      if (refresh) {
+        cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+        if (valid)
+#pragma unroll
+          for (int k = 0; k < W; ++k) {
+            st.vis[u * W + k] = vis[k];
+            st.atk[u * W + k] = atk[k];
+          }
+      }
+      env_sync<W>();
+      return;
+    }
+    cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+    double ra, re;
+    team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
+    prev_gap = ra - re;
+    own_features(S.own[i], U, hp, px, py, ch, sh, cd, alive, fw, fh);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      S.vis[i * W + k] = vis[k];
+      S.atk[i * W + k] = atk[k];
+    }
+    env_sync<W>();
+    const tabx_outputs& O = P.out;
+    if (O.observations) write_obs<W>(O.observations, b, N, P.D, S, tab, C, i);
+    if (O.global_state) write_global<W>(O.global_state, b, N, Z, P.G, S, C, i);
+    if (valid) {
+      const bool ctl = alive && U.active;
+      if (O.action_mask) {
+        uint8_t* m = O.action_mask + u * TABX_NUM_ACTIONS;
+        for (int a = 0; a < 5; ++a) m[a] = ctl;
+        m[5] = ctl && cd <= 0.0;
+        m[6] = (ctl && C->enable_noop) || !ctl;
+      }
+      if (O.rewards) O.rewards[u] = 0.0f;
+      if (O.actions) O.actions[u] = A_NOOP;
+      if (O.interactions)
+        for (int j = 0; j < N; ++j) O.interactions[u * N + j] = 0;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        st.vis[u * W + k] = vis[k];
+        st.atk[u * W + k] = atk[k];
+      }
+    }
+    if (i == 0) {
+      st.prev_gap[b] = prev_gap;
+      if (O.terminated) O.terminated[b] = (lf & F_TERM) ? 1 : 0;
+      if (O.truncated) O.truncated[b] = (lf & F_TRUNC) ? 1 : 0;
+      if (O.done) O.done[b] = (lf & F_DONE) ? 1 : 0;
+      if (O.dense_reward) O.dense_reward[b] = 0.0;
+      if (O.winner) O.winner[b] = winner;
+      if (O.reason) O.reason[b] = reason;
+      if (O.first_kill) O.first_kill[b] = fk;
+      if (O.episode_return) O.episode_return[b] = ep_ret;
+      if (O.episode_length) O.episode_length[b] = t;
+      if (O.reset_mask) O.reset_mask[b] = 0;
+    }
+    env_sync<W>();
+    return;
+  }
+
+  // ======================= step (environment.py:207-348) ==================
+  publish();
+  env_sync<W>();
+
+  // 1. pre-step action mask (arrays.py:373-387)
+  const bool ctl = alive && U.active;
+  const uint32_t mask7 = ctl ? (0x1Fu | ((cd <= 0.0) ? 0x20u : 0u) | (C->enable_noop ? 0x40u : 0u))
+                             : 0x40u;
+  // 2. action resolution (environment.py:154-204)
+  const int team = U.enemy ? 1 : 0;
+  const int ctrl = C->controller[team];
+  const bool free_u = valid && ctl && running;
+  const bool heur = free_u && ctrl == TABX_CTRL_HEURISTIC;
+  int act = A_NOOP;
+  if (free_u && P.actions) act = (int)P.actions[u];
+  if (env_any<W>(heur, S, i)) {
+    // cached vis/atk of the previous stage 8, or fresh after a batch refill
+    if (refresh) {
+      cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+    } else if (valid) {
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        vis[k] = st.vis[u * W + k];
+        atk[k] = st.atk[u * W + k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < W; ++k) vis[k] = atk[k] = 0u;
+    }
+    if (heur) {
+      const double ue = uniform53(seed, (uint64_t)(int64_t)t, TAG_EXPLORE, (uint64_t)i);
+      const double up = uniform53(seed, (uint64_t)(int64_t)t, TAG_PICK, (uint64_t)i);
+      const double stepl = (U.speed * swamp_mult(C, Z, S.zin[i], swamp_m)) * dt;
+      act = scripted_action<W>(S, C, i, N, Z, U, vis, atk, hd, cd, stepl, mask7, ue, up,
+                               C->epsilon[team], C->aggressive[team], bush_m, mx, my, memv);
+    }
+  }
+  if (free_u && ctrl == TABX_CTRL_RANDOM)
+    act = kth_legal(mask7, uniform53(seed, (uint64_t)(int64_t)t, TAG_RANDOM, (uint64_t)i));
+  if (!free_u) act = A_NOOP;
+
+  // 3-4. commanded velocity, integration, timers (environment.py:215-228)
+  const bool moving = act < 4 && alive && U.active && !U.kin;
+  const double speff = U.speed * swamp_mult(C, Z, S.zin[i], swamp_m);
+  const double vmag = moving ? speff : 0.0;
+  const int ad = act < 0 ? 0 : (act > 3 ? 3 : act);
+  const double dirx = ad == 2 ? 1.0 : (ad == 3 ? -1.0 : 0.0);
+  const double diry = ad == 0 ? 1.0 : (ad == 1 ? -1.0 : 0.0);
+  const double vux = dirx * vmag + ivx;
+  const double vuy = diry * vmag + ivy;
+  if (U.active && !U.kin && running) {
+    px = px + vux * dt;
+    py = py + vuy * dt;
+  }
+  const double tick = (U.active && running) ? dt : 0.0;
+  cd = np_max(cd - tick, 0.0);
+  rv = np_max(rv - tick, 0.0);
+  env_sync<W>();
+  S.px[i] = px;
+  S.py[i] = py;
+  env_sync<W>();
+
+  // 5. contacts: detection (physics.py:27-49), Gauss-Seidel (physics.py:52-94)
+  uint32_t trow[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) trow[k] = 0u;
+  bool any_touch = false;
+  if (valid && U.active && running) {
+    for (int j = i + 1; j < N; ++j) {
+      if (!(S.uf[j] & UF_ACTIVE)) continue;
+      const double dx = S.px[j] - px, dy = S.py[j] - py;
+      const double dist = sqrt(dx * dx + dy * dy);
+      const double rs = U.rad + S.rad[j];
+      const double depth = dist == 0.0 ? rs : rs - dist;
+      if (depth > 0.0) {
+        trow[j >> 5] |= 1u << (j & 31);
+        any_touch = true;
+      }
+    }
+  }
+  double vfx = vux, vfy = vuy;
+  if (env_any<W>(any_touch, S, i)) {
+#pragma unroll
+    for (int k = 0; k < W; ++k) S.touch[i * W + k] = trow[k];
+    S.vx[i] = vux;
+    S.vy[i] = vuy;
+    S.sx[i] = 0.0;
+    S.sy[i] = 0.0;
+    env_sync<W>();
+    if (i == 0) {
+      const double e = C->restitution, slop = C->slop, beta = C->correction;
+      for (int a = 0; a < N; ++a) {
+        for (int k = 0; k < W; ++k) {
+          uint32_t m = S.touch[a * W + k];
+          while (m) {
+            const int bb = (k << 5) + __ffs(m) - 1;
+            m &= m - 1;
+            const double wa = C->inv_mass[a], wb = C->inv_mass[bb];
+            const double w = wa + wb;
+            if (!(w > 0.0)) continue;
+            const double dx = S.px[bb] - S.px[a], dy = S.py[bb] - S.py[a];
+            const double dist = sqrt(dx * dx + dy * dy);
+            const double rs = S.rad[a] + S.rad[bb];
+            const bool coinc = dist == 0.0;
+            const double depth = coinc ? rs : rs - dist;
+            const double nx = coinc ? 1.0 : dx / dist;
+            const double ny = coinc ? 0.0 : dy / dist;
+            const double rel = (S.vx[bb] - S.vx[a]) * nx + (S.vy[bb] - S.vy[a]) * ny;
+            const double jm = rel <= 0.0 ? (-(1.0 + e) * rel) / w : 0.0;
+            S.vx[a] = S.vx[a] - (jm * wa) * nx;
+            S.vy[a] = S.vy[a] - (jm * wa) * ny;
+            S.vx[bb] = S.vx[bb] + (jm * wb) * nx;
+            S.vy[bb] = S.vy[bb] + (jm * wb) * ny;
+            const double corr = (beta * np_max(depth - slop, 0.0)) / w;
+            S.sx[a] = S.sx[a] - (corr * wa) * nx;
+            S.sy[a] = S.sy[a] - (corr * wa) * ny;
+            S.sx[bb] = S.sx[bb] + (corr * wb) * nx;
+            S.sy[bb] = S.sy[bb] + (corr * wb) * ny;
+          }
+        }
+      }
+    }
+    env_sync<W>();
+    vfx = S.vx[i];
+    vfy = S.vy[i];
+    px = px + S.sx[i];
+    py = py + S.sy[i];
+  }
+  if (running) {
+    ivx = vfx - vux;
+    ivy = vfy - vuy;
+    vlx = vfx;
+    vly = vfy;
+  }
+
+  // 6. boundary penalty + clip (physics.py:97-120)
+  if (running && valid) {
+    const bool out = px < 0.0 || px > fw || py < 0.0 || py > fh;
+    if (out && alive && U.active) hp = np_max(hp - (C->boundary_coeff * U.mh) * dt, 0.0);
+    if (U.active && !U.kin) {
+      px = np_clip(px, 0.0, fw);
+      py = np_clip(py, 0.0, fh);
+    }
+  }
+  // 7. rotation (environment.py:249-252)
+  if (act == A_ROTATE && alive && U.active && running) {
+    hd = np_remainder(hd + C->rot_step, 6.283185307179586);
+    ch = libm_cos(hd);
+    sh = libm_sin(hd);
+  }
+
+  // 8. caches at the post-move state (environment.py:254-257)
+  env_sync<W>();
+  publish();
+  env_sync<W>();
+  cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+
+  // 9. combat (combat.py:86-113; environment.py:259-265)
+  const bool swing = act == A_ATTACK && alive && U.active && cd <= 0.0;
+  const bool landed = running && swing && tgt >= 0;
+  S.tgt[i] = landed ? tgt : -1;
+  env_sync<W>();
+  double delta = 0.0;
+  bool was_hit = false;
+  for (int a = 0; a < N; ++a) {
+    if (S.tgt[a] == i) {
+      delta += S.dmg[a];
+      was_hit = true;
+    }
+  }
+  if (running) {
+    if (U.active && alive) hp = np_clip(hp - delta, 0.0, U.mh);
+    if (swing) cd = U.ucd;
+  }
+  // 10. reveal on contact (environment.py:267-268)
+  if (landed || was_hit) rv = C->reveal_duration;
+  // 11. lava (environment.py:270-277)
+  if (alive && U.active && running && valid) {
+    const double burn = lava_sum(C, Z, S.zin[i], lava_m) * dt;
+    hp = np_clip(hp - burn, 0.0, U.mh);
+  }
+  // 12. deaths, first kill (environment.py:279-286)
+  const bool still = alive && hp > 0.0;
+  const bool died = alive && !still;
+  alive = still;
+  const bool any_died = env_any<W>(died, S, i);
+  const bool ally_died = env_any<W>(died && !U.enemy, S, i);
+  if (any_died && fk < 0) fk = ally_died ? ENEMY : ALLY;
+
+  // rewards and termination (environment.py:288-328)
+  double ra, re;
+  team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
+  const double gap = ra - re;
+  const double dense = running ? gap - prev_gap : 0.0;
+  if (running) {
+    prev_gap = gap;
+    t += 1;
+  }
+  const int na = env_count<W>(alive && U.active && !U.enemy, S, i);
+  const int ne = env_count<W>(alive && U.active && U.enemy, S, i);
+  const bool elim = running && (na == 0 || ne == 0);
+  const bool trunc = running && !elim && t >= C->max_steps;
+  int win = -1, why = R_NONE;
+  if (elim) {
+    win = (ne == 0 && na > 0) ? ALLY : ENEMY;
+    why = R_ELIM;
+  } else if (trunc) {
+    win = ra > re ? ALLY : ENEMY;
+    why = ra == re ? R_TIE : R_TRUNC;
+  }
+  const bool fin = elim || trunc;
+  const double terminal = fin ? (win == ALLY ? 1.0 : -1.0) : 0.0;
+  const double ally_reward = dense + terminal;
+  ep_ret = ep_ret + (running ? ally_reward : 0.0);
+  if (elim) lf |= F_TERM;
+  if (trunc) lf |= F_TRUNC;
+  if (fin) {
+    lf |= F_DONE;
+    winner = win;
+    reason = why;
+  }
+  const double reward_i =
+      ((U.enemy ? -1.0 : 1.0) * (U.active ? 1.0 : 0.0)) * (running ? ally_reward : 0.0);
+
+  // ---- outputs of this step (observation uses stage-8 caches, post-step state)
+  const tabx_outputs& O = P.out;
+  const bool resets = P.auto_reset && (lf & F_DONE);
+  own_features(S.own[i], U, hp, px, py, ch, sh, cd, alive, fw, fh);
+  S.uf[i] = (S.uf[i] & ~UF_ALIVE) | (alive ? UF_ALIVE : 0u);
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    S.vis[i * W + k] = vis[k];
+    S.atk[i * W + k] = atk[k];
+  }
+  env_sync<W>();
+  {
+    float* ob = resets ? O.final_observations : O.observations;
+    float* gb = resets ? O.final_global_state : O.global_state;
+    if (ob) write_obs<W>(ob, b, N, P.D, S, tab, C, i);
+    if (gb) write_global<W>(gb, b, N, Z, P.G, S, C, i);
+  }
+  if (valid) {
+    if (O.rewards) O.rewards[u] = (float)reward_i;
+    if (O.actions) O.actions[u] = act;
+    if (O.interactions)
+      for (int j = 0; j < N; ++j) O.interactions[u * N + j] = (landed && tgt == j) ? 1 : 0;
+    if (O.action_mask && !resets) {
+      const bool c2 = alive && U.active;
+      uint8_t* m = O.action_mask + u * TABX_NUM_ACTIONS;
+      for (int a = 0; a < 5; ++a) m[a] = c2;
+      m[5] = c2 && cd <= 0.0;
+      m[6] = (c2 && C->enable_noop) || !c2;
+    }
+  }
+  if (i == 0) {
+    if (O.terminated) O.terminated[b] = (lf & F_TERM) ? 1 : 0;
+    if (O.truncated) O.truncated[b] = (lf & F_TRUNC) ? 1 : 0;
+    if (O.done) O.done[b] = (lf & F_DONE) ? 1 : 0;
+    if (O.dense_reward) O.dense_reward[b] = dense;
+    if (O.winner) O.winner[b] = winner;
+    if (O.reason) O.reason[b] = reason;
+    if (O.first_kill) O.first_kill[b] = fk;
+    if (O.episode_return) O.episode_return[b] = ep_ret;
+    if (O.episode_length) O.episode_length[b] = t;
+    if (O.reset_mask) O.reset_mask[b] = resets ? 1 : 0;
+    if (fin) {
+      st.st_episodes[b] += 1;
+      st.st_wins[b] += (win == ALLY) ? 1 : 0;
+      st.st_fk_ally[b] += (fk == ALLY) ? 1 : 0;
+      st.st_ties[b] += (why == R_TIE) ? 1 : 0;
+      st.st_elims[b] += elim ? 1 : 0;
+      st.st_len[b] += t;
+      st.st_ret[b] += ep_ret;
+    }
+  }
+
+  if (resets) {
+    // auto-reset (environment.py:502-517): reseed, respawn, fresh caches
+    env_sync<W>();
+    const int64_t episode = st.episode[b] + 1;
+    seed = key_hash(seed, (uint64_t)episode, TAG_RESEED, 0);
+    if (valid && U.active) {
+      px = C->spawn_x[i];
+      py = C->spawn_y[i];
+      hd = C->spawn_heading[i];
+      hp = U.mh;
+      alive = true;
+    } else {
+      alive = false;
+    }
+    ivx = ivy = vlx = vly = 0.0;
+    cd = rv = 0.0;
+    mx = my = 0.0;
+    memv = false;
+    t = 0;
+    ep_ret = 0.0;
+    lf = 0;
+    winner = -1;
+    reason = R_NONE;
+    fk = -1;
+    ch = libm_cos(hd);
+    sh = libm_sin(hd);
+    publish();
+    env_sync<W>();
+    cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+    team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
+    prev_gap = ra - re;
+    own_features(S.own[i], U, hp, px, py, ch, sh, cd, alive, fw, fh);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      S.vis[i * W + k] = vis[k];
+      S.atk[i * W + k] = atk[k];
+    }
+    env_sync<W>();
+    if (O.observations) write_obs<W>(O.observations, b, N, P.D, S, tab, C, i);
+    if (O.global_state) write_global<W>(O.global_state, b, N, Z, P.G, S, C, i);
+    if (valid && O.action_mask) {
+      const bool c2 = alive && U.active;
+      uint8_t* m = O.action_mask + u * TABX_NUM_ACTIONS;
+      for (int a = 0; a < 5; ++a) m[a] = c2;
+      m[5] = c2 && cd <= 0.0;
+      m[6] = (c2 && C->enable_noop) || !c2;
+    }
+    if (i == 0) {
+      st.episode[b] = episode;
+      st.seed[b] = seed;
+      P.sync->refresh[(step_no + 1) % 3] = 1;
+    }
+  }
+
+  // ---- state write-back
+  if (valid) {
+    st.pos[u] = make_double2(px, py);
+    st.heading[u] = hd;
+    st.vel[u] = make_double2(vlx, vly);
+    st.imp_dv[u] = make_double2(ivx, ivy);
+    st.health[u] = hp;
+    st.cooldown[u] = cd;
+    st.reveal[u] = rv;
+    st.mem_pos[u] = make_double2(mx, my);
+    st.ubits[u] = (alive ? U_ALIVE : 0) | (memv ? U_MEMV : 0);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      st.vis[u * W + k] = vis[k];
+      st.atk[u * W + k] = atk[k];
+    }
+  }
+  if (i == 0) {
+    st.t[b] = t;
+    st.prev_gap[b] = prev_gap;
+    st.ep_return[b] = ep_ret;
+    st.flags[b] = lf;
+    st.winner[b] = (int8_t)winner;
+    st.reason[b] = (int8_t)reason;
+    st.first_kill[b] = (int8_t)fk;
+  }
+  env_sync<W>();
+}
+
+template <int W, int EPB>
+__global__ void __launch_bounds__(32 * W * EPB) lane_kernel(const Params P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int D = P.D;
+  uint16_t* tab = reinterpret_cast<uint16_t*>(smem_raw);
+  const size_t tab_bytes = ((size_t)D * 2 + 15) & ~(size_t)15;
+  EnvSmem<W>* envs = reinterpret_cast<EnvSmem<W>*>(smem_raw + tab_bytes);
+  for (int c = threadIdx.x; c < D; c += blockDim.x) tab[c] = column_desc(c, P.N);
+  __syncthreads();
+
+  uint32_t step_no = 0;
+  bool refresh = false;
+  if (P.mode == MODE_STEP) {
+    if (P.sync->err_index != NO_ERROR) return;  // an action violated the mask: no mutation
+    step_no = P.sync->step;
+    refresh = P.sync->refresh[step_no % 3] != 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.sync->refresh[(step_no + 2) % 3] = 0;
+  } else if (P.mode == MODE_REFRESH) {
+    step_no = P.sync->step;
+    refresh = P.sync->refresh[step_no % 3] != 0;
+  }
+  const int g = threadIdx.x / (32 * W);
+  const int i = threadIdx.x % (32 * W);
+  for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB)
+    run_lane<W>(P, b, i, envs[g], tab, refresh, step_no);
+
+  if (P.mode == MODE_STEP) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const uint32_t ticket = atomicAdd(&P.sync->blocks_done, 1u);
+      if (ticket == gridDim.x - 1) {
+        P.sync->blocks_done = 0;
+        P.sync->step = step_no + 1;
+        __threadfence();
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ launchers --
+template <int W, int EPB>
+cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream,
+                                  int* grid_out) {
+  const int threads = 32 * W * EPB;
+  const size_t tab_bytes = ((size_t)P.D * 2 + 15) & ~(size_t)15;
+  const size_t smem = tab_bytes + sizeof(EnvSmem<W>) * EPB;
+  cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lane_kernel<W, EPB>, threads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  int64_t need = (P.B + EPB - 1) / EPB;
+  int64_t cap = (int64_t)sm_count * per_sm;
+  int grid = (int)(need < cap ? need : cap);
+  if (grid < 1) grid = 1;
+  if (grid_out) *grid_out = grid;
+  lane_kernel<W, EPB><<<grid, threads, smem, stream>>>(P);
+  return cudaGetLastError();
+}
+
+}  // namespace tabx

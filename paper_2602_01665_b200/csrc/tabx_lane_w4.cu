@@ -1,0 +1,8 @@
+// Lane-kernel instantiation for W = 4 (128 threads per environment).
+#include "tabx_lane.cuh"
+
+namespace tabx {
+cudaError_t launch_lanes_w4(const Params& P, int sm_count, cudaStream_t stream, int* grid) {
+  return launch_lanes_t<4, 1>(P, sm_count, stream, grid);
+}
+}  // namespace tabx
