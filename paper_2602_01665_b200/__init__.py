@@ -18,10 +18,10 @@ __version__ = "0.1.0"
 
 
 def __getattr__(name):
+    import importlib
+
     if name in ("BatchSim", "BatchOutput"):
-        from . import sim
-        return getattr(sim, name)
-    if name == "bindings":
-        from . import bindings
-        return bindings
+        return getattr(importlib.import_module(".sim", __name__), name)
+    if name in ("bindings", "sim"):
+        return importlib.import_module("." + name, __name__)
     raise AttributeError(name)
