@@ -100,6 +100,14 @@ static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
   P.G = h->G;
   P.auto_reset = h->auto_reset;
   P.mode = mode;
+  // observation staging: R rows per chunk, two buffers per environment
+  const int budget = h->W == 1 ? 6144 : 16384;
+  int R = budget / (4 * h->D);
+  if (R < 1) R = 1;
+  if (R > h->N) R = h->N;
+  int need = (R * h->D > h->G ? R * h->D : h->G) + 3;
+  P.stage_rows = R;
+  P.stage_floats = (need + 3) & ~3;
   return P;
 }
 

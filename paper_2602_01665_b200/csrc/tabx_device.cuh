@@ -79,6 +79,8 @@ struct Params {
   int N, Z, D, G;
   int auto_reset;
   int mode;
+  int stage_rows;    // observation rows per staged chunk
+  int stage_floats;  // floats per stage buffer (multiple of 4)
 };
 
 }  // namespace tabx

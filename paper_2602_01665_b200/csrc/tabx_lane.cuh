@@ -226,170 +226,230 @@ __device__ __forceinline__ UnitStatic load_static(const tabx_config* __restrict_
 
 // Visibility / attackable rows of observer i and its nearest attackable
 // target (perception.py:52-96, combat.py:16-83).  Reads positions, headings,
-// reveal timers, flags and zone bits of every unit from shared memory.
+// reveal timers, flags and zone bits of every unit from shared memory and
+// writes the two N-bit rows to S.vis / S.atk; returns the target or -1.
 template <int W>
-__device__ __forceinline__ void cache_row(const EnvSmem<W>& S, int i, int N, const UnitStatic& U,
-                                          uint32_t uf_i, uint32_t bush_m, uint32_t (&vis)[W],
-                                          uint32_t (&atk)[W], int& tgt) {
+__device__ __noinline__ int cache_row(EnvSmem<W>& S, int i, int N, double cos_half,
+                                      double srange, double dmg, double reach, double rad,
+                                      uint32_t bush_m) {
+  uint32_t vis[W], atk[W];
 #pragma unroll
   for (int k = 0; k < W; ++k) vis[k] = atk[k] = 0u;
-  tgt = -1;
-  const double px = S.px[i], py = S.py[i], ch = S.ch[i], sh = S.sh[i];
+  int tgt = -1;
+  const uint32_t uf_i = S.uf[i];
   const bool act_i = (uf_i & UF_ACTIVE) != 0;
-  const bool live_i = act_i && (uf_i & UF_ALIVE);
-  const bool enemy_i = (uf_i & UF_ENEMY) != 0;
-  const uint32_t bush_i = S.zin[i] & bush_m;
-  double best = 0.0;
-  if (!act_i) return;  // vis requires both active; atk requires vis
-  for (int j = 0; j < N; ++j) {
-    const uint32_t uj = S.uf[j];
-    if (!(uj & UF_ACTIVE)) continue;
-    const double dx = S.px[j] - px;
-    const double dy = S.py[j] - py;
-    const double dist = sqrt(dx * dx + dy * dy);
-    const double lx = dx * ch + dy * sh;
-    const double cdev = dist > 0.0 ? lx / dist : 1.0;
-    const bool wedge = cdev >= U.cos_half;
-    if (!(dist <= U.srange && wedge)) continue;
-    const bool foe = ((uj & UF_ENEMY) != 0) != enemy_i;
-    const uint32_t bush_j = S.zin[j] & bush_m;
-    const bool hidden = bush_j != 0u && foe && (bush_i & bush_j) == 0u && S.rv[j] <= 0.0;
-    if (hidden) continue;
-    vis[j >> 5] |= 1u << (j & 31);
-    const bool role = U.dmg > 0.0 ? foe : (U.dmg < 0.0 && !foe);
-    if (!(role && live_i && (uj & UF_ALIVE) && j != i)) continue;
-    const double ly = (-dx) * sh + dy * ch;
-    const double cx = np_clip(lx, 0.0, U.range);
-    const double cy = np_clip(ly, -U.rad, U.rad);
-    const double gx = lx - cx, gy = ly - cy;
-    const double rj = S.rad[j];
-    if (gx * gx + gy * gy <= rj * rj) {
-      atk[j >> 5] |= 1u << (j & 31);
-      if (tgt < 0 || dist < best) {
-        best = dist;
-        tgt = j;
+  if (act_i) {  // vis requires both active; atk requires vis
+    const double px = S.px[i], py = S.py[i], ch = S.ch[i], sh = S.sh[i];
+    const bool live_i = (uf_i & UF_ALIVE) != 0;
+    const bool enemy_i = (uf_i & UF_ENEMY) != 0;
+    const uint32_t bush_i = S.zin[i] & bush_m;
+    double best = 0.0;
+    for (int j = 0; j < N; ++j) {
+      const uint32_t uj = S.uf[j];
+      if (!(uj & UF_ACTIVE)) continue;
+      const double dx = S.px[j] - px;
+      const double dy = S.py[j] - py;
+      const double dist = sqrt(dx * dx + dy * dy);
+      const double lx = dx * ch + dy * sh;
+      const double cdev = dist > 0.0 ? lx / dist : 1.0;
+      const bool wedge = cdev >= cos_half;
+      if (!(dist <= srange && wedge)) continue;
+      const bool foe = ((uj & UF_ENEMY) != 0) != enemy_i;
+      const uint32_t bush_j = S.zin[j] & bush_m;
+      const bool hidden = bush_j != 0u && foe && (bush_i & bush_j) == 0u && S.rv[j] <= 0.0;
+      if (hidden) continue;
+      vis[j >> 5] |= 1u << (j & 31);
+      const bool role = dmg > 0.0 ? foe : (dmg < 0.0 && !foe);
+      if (!(role && live_i && (uj & UF_ALIVE) && j != i)) continue;
+      const double ly = (-dx) * sh + dy * ch;
+      const double cx = np_clip(lx, 0.0, reach);
+      const double cy = np_clip(ly, -rad, rad);
+      const double gx = lx - cx, gy = ly - cy;
+      const double rj = S.rad[j];
+      if (gx * gx + gy * gy <= rj * rj) {
+        atk[j >> 5] |= 1u << (j & 31);
+        if (tgt < 0 || dist < best) {
+          best = dist;
+          tgt = j;
+        }
       }
     }
   }
-}
-
-// Column descriptors of one observation row: kind<<13 | payload.
-//  kind 0: own feature f;  kind 1: other block k (j = k or k+1), feature f
-//  (payload k<<5 | f);  kind 2: zone z feature f (payload z<<3 | f).
-__device__ __forceinline__ uint16_t column_desc(int c, int N) {
-  if (c < TABX_OWN_DIM) return (uint16_t)c;
-  int o = c - TABX_OWN_DIM;
-  if (o < (N - 1) * TABX_OTHER_DIM) {
-    int k = o / TABX_OTHER_DIM, f = o - k * TABX_OTHER_DIM;
-    return (uint16_t)((1 << 13) | (k << 5) | f);
-  }
-  o -= (N - 1) * TABX_OTHER_DIM;
-  int z = o / TABX_ZONE_DIM, f = o - z * TABX_ZONE_DIM;
-  return (uint16_t)((2 << 13) | (z << 3) | f);
-}
-
-// One observation element (perception.py:159-192).
-template <int W>
-__device__ __forceinline__ float obs_value(const EnvSmem<W>& S, const uint16_t* __restrict__ tab,
-                                           const tabx_config* __restrict__ C, int i, int c,
-                                           double fw, double fh) {
-  if (!(S.uf[i] & UF_ACTIVE)) return 0.0f;
-  const uint32_t d = tab[c];
-  const uint32_t kind = d >> 13;
-  if (kind == 0) return S.own[i][d];
-  if (kind == 1) {
-    const int k = (d >> 5) & 255, f = d & 31;
-    const int j = k + (k >= i ? 1 : 0);
-    if (!(bit_of(&S.vis[i * W], j) && (S.uf[j] & UF_ACTIVE))) return 0.0f;
-    if (f == 2) return __double2float_rn((S.px[j] - S.px[i]) / fw);
-    if (f == 3) return __double2float_rn((S.py[j] - S.py[i]) / fh);
-    if (f == 15) return (S.uf[j] & UF_ENEMY) ? 1.0f : 0.0f;
-    if (f == 16) return bit_of(&S.atk[i * W], j) ? 1.0f : 0.0f;
-    return S.own[j][f];
-  }
-  const int z = (d >> 3) & 31, f = d & 7;
-  const int ty = C->zone_type[z];
-  if (ty == TABX_ZONE_NONE) return 0.0f;
-  switch (f) {
-    case 0: case 1: case 2: return ty == f + 1 ? 1.0f : 0.0f;
-    case 3: return __double2float_rn((C->zone_cx[z] - S.px[i]) / fw);
-    case 4: return __double2float_rn((C->zone_cy[z] - S.py[i]) / fh);
-    case 5: return __double2float_rn(C->zone_ax[z]);
-    case 6: return __double2float_rn(C->zone_ay[z]);
-    default: return __double2float_rn(C->zone_effect[z]);
-  }
-}
-
-// Stream the env's [N, D] observation block (flat, 16-byte stores in the
-// aligned body, scalar head/tail when N*D is not a multiple of 4).
-template <int W>
-__device__ __forceinline__ void write_obs(float* __restrict__ dst, int64_t b, int N, int D,
-                                          const EnvSmem<W>& S, const uint16_t* __restrict__ tab,
-                                          const tabx_config* __restrict__ C, int tid) {
-  constexpr int NT = 32 * W;
-  const int64_t E = (int64_t)N * D;
-  const int64_t start = b * E;
-  const double fw = C->field_w, fh = C->field_h;
-  int head = (int)((4 - (start & 3)) & 3);
-  if (head > E) head = (int)E;
-  for (int e = tid; e < head; e += NT) {
-    int i = e / D, c = e - i * D;
-    dst[start + e] = obs_value<W>(S, tab, C, i, c, fw, fh);
-  }
-  const int64_t nvec = (E - head) >> 2;
-  float4* __restrict__ v4 = reinterpret_cast<float4*>(dst + start + head);
-  for (int64_t q = tid; q < nvec; q += NT) {
-    int e0 = head + (int)(q << 2);
-    int i = e0 / D, c = e0 - i * D;
-    float r[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      r[k] = obs_value<W>(S, tab, C, i, c, fw, fh);
-      if (++c == D) {
-        c = 0;
-        ++i;
-      }
-    }
-    __stcs(v4 + q, make_float4(r[0], r[1], r[2], r[3]));
+  for (int k = 0; k < W; ++k) {
+    S.vis[i * W + k] = vis[k];
+    S.atk[i * W + k] = atk[k];
   }
-  for (int64_t e = head + (nvec << 2) + tid; e < E; e += NT) {
-    int i = (int)(e / D), c = (int)(e - (int64_t)i * D);
-    dst[start + e] = obs_value<W>(S, tab, C, i, c, fw, fh);
+  return tgt;
+}
+
+template <int W>
+__device__ __forceinline__ int cache_row_of(EnvSmem<W>& S, int i, int N, const UnitStatic& U,
+                                            uint32_t bush_m) {
+  return cache_row<W>(S, i, N, U.cos_half, U.srange, U.dmg, U.range, U.rad, bush_m);
+}
+
+// ------------------------------------------------ observation streaming --
+// Observation rows are assembled in shared memory (one thread per (observer,
+// other) pair block, one per own / zone block) and leave through TMA bulk
+// stores (cp.async.bulk.global.shared::cta), double-buffered so the fill of
+// chunk c+1 overlaps the store of chunk c.  The 16-byte aligned interior of
+// each chunk goes by TMA; the <= 3-float head and tail by plain stores.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_s2g(void* g, const void* s, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g),
+               "r"(smem_addr(s)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+}
+template <int K>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(K) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// dst[gs, gs+count) <- stage[pad, pad+count), pad = gs & 3.
+template <int W>
+__device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs, int count,
+                                            const float* stage, int tid) {
+  constexpr int NT = 32 * W;
+  const int pad = (int)(gs & 3);
+  const int64_t a0 = (gs + 3) & ~(int64_t)3;
+  const int64_t a1 = (gs + count) & ~(int64_t)3;
+  if (a1 > a0) {
+    if (tid == 0) {
+      bulk_s2g(dst + a0, stage + pad + (a0 - gs), (uint32_t)((a1 - a0) * 4));
+      bulk_commit();
+    }
+    for (int e = tid; e < (int)(a0 - gs); e += NT) dst[gs + e] = stage[pad + e];
+    for (int e = (int)(a1 - gs) + tid; e < count; e += NT) dst[gs + e] = stage[pad + e];
+  } else {
+    for (int e = tid; e < count; e += NT) dst[gs + e] = stage[pad + e];
   }
 }
 
-// Global state row (perception.py:194-200): own blocks then absolute zones.
+// Observation rows of one environment (perception.py:159-192) and its
+// global-state row (perception.py:194-200), from S.own / S.vis / S.atk /
+// positions.  R rows per chunk; SF floats per stage buffer.
 template <int W>
-__device__ __forceinline__ void write_global(float* __restrict__ dst, int64_t b, int N, int Z,
-                                             int G, const EnvSmem<W>& S,
-                                             const tabx_config* __restrict__ C, int tid) {
+__device__ __noinline__ void emit_observations(float* __restrict__ obs, float* __restrict__ glob,
+                                               int64_t b, int N, int Z, int D, int G, int R,
+                                               int SF, EnvSmem<W>& S, float* stage,
+                                               const tabx_config* __restrict__ C, int tid) {
   constexpr int NT = 32 * W;
-  float* row = dst + b * (int64_t)G;
-  const int own_cols = N * TABX_OWN_DIM;
-  for (int c = tid; c < G; c += NT) {
-    float v;
-    if (c < own_cols) {
-      int i = c / TABX_OWN_DIM, f = c - i * TABX_OWN_DIM;
-      v = S.own[i][f];
-    } else {
-      int o = c - own_cols;
-      int z = o >> 3, f = o & 7;
-      int ty = C->zone_type[z];
+  const double fw = C->field_w, fh = C->field_h;
+  const int M = N - 1;
+  const int zoff = TABX_OWN_DIM + TABX_OTHER_DIM * M;
+  int buf = 0;
+  if (obs) {
+    for (int r0 = 0; r0 < N; r0 += R) {
+      const int nr = min(R, N - r0);
+      const int64_t gs = (b * N + r0) * (int64_t)D;
+      float* st = stage + buf * SF;
+      float* row0 = st + (int)(gs & 3);
+      if (tid == 0) bulk_wait_read<1>();
+      env_sync<W>();
+      for (int e = tid; e < nr * TABX_OWN_DIM; e += NT) {
+        const int rr = e / TABX_OWN_DIM, f = e - rr * TABX_OWN_DIM;
+        row0[rr * D + f] = S.own[r0 + rr][f];
+      }
+      if (M > 0) {
+        const int qd = NT / M, qm = NT % M;
+        int rr = tid / M, k = tid - (tid / M) * M;
+        for (int p = tid; p < nr * M; p += NT) {
+          const int r = r0 + rr;
+          const int j = k + (k >= r ? 1 : 0);
+          float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * k;
+          const uint32_t uj = S.uf[j];
+          const bool show = (S.uf[r] & UF_ACTIVE) && bit_of(&S.vis[r * W], j) && (uj & UF_ACTIVE);
+          if (show) {
+            const float* oj = S.own[j];
+            blk[0] = oj[0];
+            blk[1] = oj[1];
+            blk[2] = __double2float_rn((S.px[j] - S.px[r]) / fw);
+            blk[3] = __double2float_rn((S.py[j] - S.py[r]) / fh);
+#pragma unroll
+            for (int f = 4; f < TABX_OWN_DIM; ++f) blk[f] = oj[f];
+            blk[15] = (uj & UF_ENEMY) ? 1.0f : 0.0f;
+            blk[16] = bit_of(&S.atk[r * W], j) ? 1.0f : 0.0f;
+          } else {
+#pragma unroll
+            for (int f = 0; f < TABX_OTHER_DIM; ++f) blk[f] = 0.0f;
+          }
+          rr += qd;
+          k += qm;
+          if (k >= M) {
+            k -= M;
+            ++rr;
+          }
+        }
+      }
+      for (int q = tid; q < nr * Z; q += NT) {
+        const int rr = q / Z, z = q - rr * Z;
+        const int r = r0 + rr;
+        float* blk = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
+        const int ty = C->zone_type[z];
+        if (ty != TABX_ZONE_NONE && (S.uf[r] & UF_ACTIVE)) {
+          blk[0] = ty == 1 ? 1.0f : 0.0f;
+          blk[1] = ty == 2 ? 1.0f : 0.0f;
+          blk[2] = ty == 3 ? 1.0f : 0.0f;
+          blk[3] = __double2float_rn((C->zone_cx[z] - S.px[r]) / fw);
+          blk[4] = __double2float_rn((C->zone_cy[z] - S.py[r]) / fh);
+          blk[5] = __double2float_rn(C->zone_ax[z]);
+          blk[6] = __double2float_rn(C->zone_ay[z]);
+          blk[7] = __double2float_rn(C->zone_effect[z]);
+        } else {
+#pragma unroll
+          for (int f = 0; f < TABX_ZONE_DIM; ++f) blk[f] = 0.0f;
+        }
+      }
+      fence_proxy_async();
+      env_sync<W>();
+      flush_stage<W>(obs, gs, nr * D, st, tid);
+      buf ^= 1;
+    }
+  }
+  if (glob) {
+    const int64_t gs = b * (int64_t)G;
+    float* st = stage + buf * SF;
+    float* row = st + (int)(gs & 3);
+    if (tid == 0) bulk_wait_read<1>();
+    env_sync<W>();
+    const float* own = &S.own[0][0];
+    for (int e = tid; e < N * TABX_OWN_DIM; e += NT) row[e] = own[e];
+    for (int q = tid; q < Z * TABX_ZONE_DIM; q += NT) {
+      const int z = q >> 3, f = q & 7;
+      const int ty = C->zone_type[z];
+      float v;
       if (ty == TABX_ZONE_NONE) {
         v = 0.0f;
       } else {
         switch (f) {
           case 0: case 1: case 2: v = ty == f + 1 ? 1.0f : 0.0f; break;
-          case 3: v = __double2float_rn(C->zone_cx[z] / C->field_w); break;
-          case 4: v = __double2float_rn(C->zone_cy[z] / C->field_h); break;
+          case 3: v = __double2float_rn(C->zone_cx[z] / fw); break;
+          case 4: v = __double2float_rn(C->zone_cy[z] / fh); break;
           case 5: v = __double2float_rn(C->zone_ax[z]); break;
           case 6: v = __double2float_rn(C->zone_ay[z]); break;
           default: v = __double2float_rn(C->zone_effect[z]); break;
         }
       }
+      row[N * TABX_OWN_DIM + q] = v;
     }
-    row[c] = v;
+    fence_proxy_async();
+    env_sync<W>();
+    flush_stage<W>(glob, gs, G, st, tid);
   }
+  if (tid == 0) bulk_wait_read<0>();
+  env_sync<W>();
 }
 
 // Own-feature block of unit i (perception.py:108-132) rounded to float32.
@@ -546,7 +606,7 @@ __device__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restric
 // ---------------------------------------------------------------- lane ---
 template <int W>
 __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
-                         const uint16_t* __restrict__ tab, bool refresh, uint32_t step_no) {
+                         float* stage, bool refresh, uint32_t step_no) {
   const int N = P.N, Z = P.Z;
   const bool valid = i < N;
   const int64_t u = b * N + i;
@@ -619,31 +679,31 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     env_sync<W>();
     if (P.mode == MODE_REFRESH) {
       if (refresh) {
-        cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+        cache_row_of<W>(S, i, N, U, bush_m);
         if (valid)
 #pragma unroll
           for (int k = 0; k < W; ++k) {
-            st.vis[u * W + k] = vis[k];
-            st.atk[u * W + k] = atk[k];
+            st.vis[u * W + k] = S.vis[i * W + k];
+            st.atk[u * W + k] = S.atk[i * W + k];
           }
       }
       env_sync<W>();
       return;
     }
-    cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+    cache_row_of<W>(S, i, N, U, bush_m);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      vis[k] = S.vis[i * W + k];
+      atk[k] = S.atk[i * W + k];
+    }
     double ra, re;
     team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
     prev_gap = ra - re;
     own_features(S.own[i], U, hp, px, py, ch, sh, cd, alive, fw, fh);
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      S.vis[i * W + k] = vis[k];
-      S.atk[i * W + k] = atk[k];
-    }
     env_sync<W>();
     const tabx_outputs& O = P.out;
-    if (O.observations) write_obs<W>(O.observations, b, N, P.D, S, tab, C, i);
-    if (O.global_state) write_global<W>(O.global_state, b, N, Z, P.G, S, C, i);
+    emit_observations<W>(O.observations, O.global_state, b, N, Z, P.D, P.G, P.stage_rows,
+                         P.stage_floats, S, stage, C, i);
     if (valid) {
       const bool ctl = alive && U.active;
       if (O.action_mask) {
@@ -697,7 +757,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   if (env_any<W>(heur, S, i)) {
     // cached vis/atk of the previous stage 8, or fresh after a batch refill
     if (refresh) {
-      cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+      cache_row_of<W>(S, i, N, U, bush_m);
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        vis[k] = S.vis[i * W + k];
+        atk[k] = S.atk[i * W + k];
+      }
     } else if (valid) {
 #pragma unroll
       for (int k = 0; k < W; ++k) {
@@ -834,7 +899,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   env_sync<W>();
   publish();
   env_sync<W>();
-  cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+  tgt = cache_row_of<W>(S, i, N, U, bush_m);
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    vis[k] = S.vis[i * W + k];
+    atk[k] = S.atk[i * W + k];
+  }
 
   // 9. combat (combat.py:86-113; environment.py:259-265)
   const bool swing = act == A_ATTACK && alive && U.active && cd <= 0.0;
@@ -908,17 +978,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const bool resets = P.auto_reset && (lf & F_DONE);
   own_features(S.own[i], U, hp, px, py, ch, sh, cd, alive, fw, fh);
   S.uf[i] = (S.uf[i] & ~UF_ALIVE) | (alive ? UF_ALIVE : 0u);
-#pragma unroll
-  for (int k = 0; k < W; ++k) {
-    S.vis[i * W + k] = vis[k];
-    S.atk[i * W + k] = atk[k];
-  }
   env_sync<W>();
   {
     float* ob = resets ? O.final_observations : O.observations;
     float* gb = resets ? O.final_global_state : O.global_state;
-    if (ob) write_obs<W>(ob, b, N, P.D, S, tab, C, i);
-    if (gb) write_global<W>(gb, b, N, Z, P.G, S, C, i);
+    emit_observations<W>(ob, gb, b, N, Z, P.D, P.G, P.stage_rows, P.stage_floats, S, stage, C,
+                         i);
   }
   if (valid) {
     if (O.rewards) O.rewards[u] = (float)reward_i;
@@ -983,18 +1048,18 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     sh = libm_sin(hd);
     publish();
     env_sync<W>();
-    cache_row<W>(S, i, N, U, S.uf[i], bush_m, vis, atk, tgt);
+    cache_row_of<W>(S, i, N, U, bush_m);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      vis[k] = S.vis[i * W + k];
+      atk[k] = S.atk[i * W + k];
+    }
     team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
     prev_gap = ra - re;
     own_features(S.own[i], U, hp, px, py, ch, sh, cd, alive, fw, fh);
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      S.vis[i * W + k] = vis[k];
-      S.atk[i * W + k] = atk[k];
-    }
     env_sync<W>();
-    if (O.observations) write_obs<W>(O.observations, b, N, P.D, S, tab, C, i);
-    if (O.global_state) write_global<W>(O.global_state, b, N, Z, P.G, S, C, i);
+    emit_observations<W>(O.observations, O.global_state, b, N, Z, P.D, P.G, P.stage_rows,
+                         P.stage_floats, S, stage, C, i);
     if (valid && O.action_mask) {
       const bool c2 = alive && U.active;
       uint8_t* m = O.action_mask + u * TABX_NUM_ACTIONS;
@@ -1041,12 +1106,9 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 template <int W, int EPB>
 __global__ void __launch_bounds__(32 * W * EPB) lane_kernel(const Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int D = P.D;
-  uint16_t* tab = reinterpret_cast<uint16_t*>(smem_raw);
-  const size_t tab_bytes = ((size_t)D * 2 + 15) & ~(size_t)15;
-  EnvSmem<W>* envs = reinterpret_cast<EnvSmem<W>*>(smem_raw + tab_bytes);
-  for (int c = threadIdx.x; c < D; c += blockDim.x) tab[c] = column_desc(c, P.N);
-  __syncthreads();
+  EnvSmem<W>* envs = reinterpret_cast<EnvSmem<W>*>(smem_raw);
+  const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
+  float* stages = reinterpret_cast<float*>(smem_raw + env_bytes);
 
   uint32_t step_no = 0;
   bool refresh = false;
@@ -1062,7 +1124,8 @@ __global__ void __launch_bounds__(32 * W * EPB) lane_kernel(const Params P) {
   const int g = threadIdx.x / (32 * W);
   const int i = threadIdx.x % (32 * W);
   for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB)
-    run_lane<W>(P, b, i, envs[g], tab, refresh, step_no);
+    run_lane<W>(P, b, i, envs[g], stages + (size_t)g * 2 * P.stage_floats, refresh, step_no);
+  if (i == 0) bulk_wait_all();  // bulk stores issued by this thread are complete
 
   if (P.mode == MODE_STEP) {
     __syncthreads();
@@ -1083,8 +1146,8 @@ template <int W, int EPB>
 cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream,
                                   int* grid_out) {
   const int threads = 32 * W * EPB;
-  const size_t tab_bytes = ((size_t)P.D * 2 + 15) & ~(size_t)15;
-  const size_t smem = tab_bytes + sizeof(EnvSmem<W>) * EPB;
+  const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
+  const size_t smem = env_bytes + (size_t)EPB * 2 * P.stage_floats * sizeof(float);
   cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

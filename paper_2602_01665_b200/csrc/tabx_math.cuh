@@ -20,9 +20,11 @@
 
 #if defined(__CUDACC__)
 #define TABX_HD __host__ __device__ __forceinline__
+#define TABX_HD_CALL __host__ __device__ __noinline__
 #define TABX_SC_TABLE_QUAL __device__ const
 #else
 #define TABX_HD static inline
+#define TABX_HD_CALL static
 #define TABX_SC_TABLE_QUAL static const
 #endif
 
@@ -130,7 +132,7 @@ TABX_HD double libm_do_sincos(double a, double da, int n) {
   return (n & 2) ? -r : r;
 }
 
-TABX_HD double libm_sin(double x) {
+TABX_HD_CALL double libm_sin(double x) {
   uint32_t k = (uint32_t)(d_to_bits(x) >> 32) & 0x7fffffffu;
   if (k < 0x3e500000u) return x;
   if (k < 0x3feb6000u) return libm_do_sin(x, 0.0);
@@ -143,7 +145,7 @@ TABX_HD double libm_sin(double x) {
   return sin(x);
 }
 
-TABX_HD double libm_cos(double x) {
+TABX_HD_CALL double libm_cos(double x) {
   uint32_t k = (uint32_t)(d_to_bits(x) >> 32) & 0x7fffffffu;
   if (k < 0x3e400000u) return 1.0;
   if (k < 0x3feb6000u) return libm_do_cos(x, 0.0);
