@@ -233,7 +233,7 @@ def run_gpu_arm(args) -> int:
     torch.cuda.empty_cache()
 
     # ---------------- end-to-end through the trainer API with host buffers
-    e2e_steps = max(3, min(args.steps, args.e2e_steps))
+    e2e_steps = 0 if args.no_e2e else max(3, min(args.steps, args.e2e_steps))
     doc = save_scenario(base).encode()  # ally external, enemy heuristic-medium
     h = bindings.make_batch(doc, per, args.seed, device=dev, first_lane=first,
                             interactions=False, final_observations=True)
@@ -252,7 +252,7 @@ def run_gpu_arm(args) -> int:
         trunc_h.copy_(trunc, non_blocking=True)
         stream.synchronize()
 
-    for k in range(args.warmup):
+    for k in range(args.warmup if e2e_steps else 0):
         e2e_step(k)
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -265,7 +265,7 @@ def run_gpu_arm(args) -> int:
     barrier()
     wall = time.perf_counter() - w0
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), 1000.0 * wall))
-    e2e_value = total * e2e_steps / (e2e_ms / 1000.0)
+    e2e_value = total * e2e_steps / (e2e_ms / 1000.0) if e2e_steps else None
     h.sim.close()
 
     # ---------------- CPU baseline (rank 0, N=1 only)
@@ -337,6 +337,7 @@ def main(argv=None) -> int:
     ap.add_argument("--cpu-envs", type=int, default=256)
     ap.add_argument("--cpu-steps", type=int, default=40)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -18,7 +18,8 @@ OK = 0
 E_ARGUMENT, E_CUDA, E_ACTION_MASK, E_SHAPE, E_ALIGNMENT, E_CAPACITY = 1, 2, 3, 4, 5, 6
 
 LIB_NAME = "_tabx.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+LIB_PATH = os.environ.get("TABX_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                      LIB_NAME)
 
 _d = ct.c_double
 _u8 = ct.c_uint8

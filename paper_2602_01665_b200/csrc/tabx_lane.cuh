@@ -1103,8 +1103,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   env_sync<W>();
 }
 
+#ifndef TABX_MIN_BLOCKS
+#define TABX_MIN_BLOCKS 1
+#endif
 template <int W, int EPB>
-__global__ void __launch_bounds__(32 * W * EPB) lane_kernel(const Params P) {
+__global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
+    lane_kernel(const Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EnvSmem<W>* envs = reinterpret_cast<EnvSmem<W>*>(smem_raw);
   const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;

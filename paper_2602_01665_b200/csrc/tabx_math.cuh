@@ -20,7 +20,7 @@
 
 #if defined(__CUDACC__)
 #define TABX_HD __host__ __device__ __forceinline__
-#define TABX_HD_CALL __host__ __device__ __noinline__
+#define TABX_HD_CALL static __host__ __device__ __noinline__
 #define TABX_SC_TABLE_QUAL __device__ const
 #else
 #define TABX_HD static inline
