@@ -43,10 +43,12 @@ __global__ void validate_kernel(const int64_t* __restrict__ actions, DevState st
 }
 
 // fill_env for lanes [b0, b1) (arrays.py:244-321); also used at creation.
-__global__ void spawn_kernel(DevState st, const tabx_config* __restrict__ cfgs, int64_t b0,
-                             int64_t b1, int N, int W, int reset_stats) {
+__global__ void spawn_kernel(DevState st, const tabx_config* __restrict__ cfgs,
+                             const DerivedCfg* __restrict__ dcfgs, int64_t b0, int64_t b1, int N,
+                             int W, int reset_stats) {
   for (int64_t b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
     const tabx_config* C = cfgs + st.cfg[b];
+    const DerivedCfg* DC = dcfgs + st.cfg[b];
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
       const int64_t u = b * N + i;
       if (C->active[i]) {
@@ -62,6 +64,9 @@ __global__ void spawn_kernel(DevState st, const tabx_config* __restrict__ cfgs, 
       st.cooldown[u] = 0.0;
       st.reveal[u] = 0.0;
       st.mem_pos[u] = make_double2(0.0, 0.0);
+      const double h = st.heading[u];
+      st.hcs[u] = make_double2(libm_cos(h), libm_sin(h));
+      st.zbits[u] = zone_bits(C, DC, C->n_zones, st.pos[u].x, st.pos[u].y);
       for (int k = 0; k < W; ++k) {
         st.vis[u * W + k] = 0u;
         st.atk[u * W + k] = 0u;
@@ -123,7 +128,8 @@ __global__ void export_kernel(DevState st, tabx_state d, int64_t B, int N, int W
   }
 }
 
-__global__ void import_kernel(DevState st, tabx_state s, int64_t B, int N, int W) {
+__global__ void import_kernel(DevState st, tabx_state s, const tabx_config* __restrict__ cfgs,
+                              const DerivedCfg* __restrict__ dcfgs, int64_t B, int N, int W) {
   const int64_t n = B * N;
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
        u += (int64_t)gridDim.x * blockDim.x) {
@@ -153,6 +159,15 @@ __global__ void import_kernel(DevState st, tabx_state s, int64_t B, int N, int W
     if (s.mem_pos) st.mem_pos[u] = make_double2(s.mem_pos[2 * u], s.mem_pos[2 * u + 1]);
     if (s.alive && s.mem_valid)
       st.ubits[u] = (s.alive[u] ? U_ALIVE : 0) | (s.mem_valid[u] ? U_MEMV : 0);
+    {
+      // derived caches follow the imported heading / position
+      const int32_t k = s.config ? s.config[b] : st.cfg[b];
+      const double h = s.heading ? s.heading[u] : st.heading[u];
+      const double x = s.pos ? s.pos[2 * u] : st.pos[u].x;
+      const double y = s.pos ? s.pos[2 * u + 1] : st.pos[u].y;
+      st.hcs[u] = make_double2(libm_cos(h), libm_sin(h));
+      st.zbits[u] = zone_bits(cfgs + k, dcfgs + k, cfgs[k].n_zones, x, y);
+    }
     if (s.vis && s.atk) {
       for (int k = 0; k < W; ++k) {
         uint32_t vw = 0, aw = 0;
@@ -165,6 +180,43 @@ __global__ void import_kernel(DevState st, tabx_state s, int64_t B, int N, int W
         st.vis[u * W + k] = vw;
         st.atk[u * W + k] = aw;
       }
+    }
+  }
+}
+
+// Per-config derived values (reciprocals, masks, roster sizes).
+__global__ void derive_kernel(const tabx_config* __restrict__ cfgs, DerivedCfg* dcfgs, int k0,
+                              int k1) {
+  for (int k = k0 + blockIdx.x; k < k1; k += gridDim.x) {
+    const tabx_config* C = cfgs + k;
+    DerivedCfg* D = dcfgs + k;
+    for (int i = threadIdx.x; i < C->n_units; i += blockDim.x) {
+      D->rmh[i] = 1.0 / C->max_health[i];
+      D->rucd[i] = C->cooldown[i] > 0.0 ? 1.0 / C->cooldown[i] : 0.0;
+    }
+    for (int z = threadIdx.x; z < C->n_zones; z += blockDim.x) {
+      D->rax[z] = C->zone_type[z] ? 1.0 / C->zone_ax[z] : 0.0;
+      D->ray[z] = C->zone_type[z] ? 1.0 / C->zone_ay[z] : 0.0;
+    }
+    if (threadIdx.x == 0) {
+      D->rw = 1.0 / C->field_w;
+      D->rh = 1.0 / C->field_h;
+      uint32_t lm = 0, bm = 0, sm = 0;
+      for (int z = 0; z < C->n_zones; ++z) {
+        if (C->zone_type[z] == TABX_ZONE_LAVA) lm |= 1u << z;
+        if (C->zone_type[z] == TABX_ZONE_BUSH) bm |= 1u << z;
+        if (C->zone_type[z] == TABX_ZONE_SWAMP) sm |= 1u << z;
+      }
+      D->lava_m = lm;
+      D->bush_m = bm;
+      D->swamp_m = sm;
+      int na = 0, ne = 0;
+      for (int i = 0; i < C->n_units; ++i) {
+        if (!C->active[i]) continue;
+        if (C->team[i]) ++ne; else ++na;
+      }
+      D->n_ally = na;
+      D->n_enemy = ne;
     }
   }
 }
@@ -230,12 +282,13 @@ cudaError_t launch_validate(const int64_t* actions, const DevState& st, const ta
   return cudaGetLastError();
 }
 
-cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, int64_t b0, int64_t b1,
-                         int N, int W, int reset_stats, int sm_count, cudaStream_t stream) {
+cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const DerivedCfg* dcfgs,
+                         int64_t b0, int64_t b1, int N, int W, int reset_stats, int sm_count,
+                         cudaStream_t stream) {
   int64_t n = b1 - b0;
   int grid = (int)(n < (int64_t)sm_count * 32 ? n : (int64_t)sm_count * 32);
   if (grid < 1) return cudaSuccess;
-  spawn_kernel<<<grid, 32 * W, 0, stream>>>(st, cfgs, b0, b1, N, W, reset_stats);
+  spawn_kernel<<<grid, 32 * W, 0, stream>>>(st, cfgs, dcfgs, b0, b1, N, W, reset_stats);
   return cudaGetLastError();
 }
 
@@ -245,9 +298,17 @@ cudaError_t launch_export(const DevState& st, const tabx_state& d, int64_t B, in
   return cudaGetLastError();
 }
 
-cudaError_t launch_import(const DevState& st, const tabx_state& s, int64_t B, int N, int W,
-                          int sm_count, cudaStream_t stream) {
-  import_kernel<<<grid_for(B * N, 256, sm_count), 256, 0, stream>>>(st, s, B, N, W);
+cudaError_t launch_import(const DevState& st, const tabx_state& s, const tabx_config* cfgs,
+                          const DerivedCfg* dcfgs, int64_t B, int N, int W, int sm_count,
+                          cudaStream_t stream) {
+  import_kernel<<<grid_for(B * N, 256, sm_count), 256, 0, stream>>>(st, s, cfgs, dcfgs, B, N, W);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_derive(const tabx_config* cfgs, DerivedCfg* dcfgs, int k0, int k1,
+                          cudaStream_t stream) {
+  if (k1 <= k0) return cudaSuccess;
+  derive_kernel<<<k1 - k0, 128, 0, stream>>>(cfgs, dcfgs, k0, k1);
   return cudaGetLastError();
 }
 

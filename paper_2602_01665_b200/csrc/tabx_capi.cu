@@ -13,12 +13,16 @@ namespace tabx {
 cudaError_t launch_lanes(const Params& P, int W, int sm_count, cudaStream_t stream, int* grid);
 cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
                             int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream);
-cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, int64_t b0, int64_t b1,
-                         int N, int W, int reset_stats, int sm_count, cudaStream_t stream);
+cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const DerivedCfg* dcfgs,
+                         int64_t b0, int64_t b1, int N, int W, int reset_stats, int sm_count,
+                         cudaStream_t stream);
+cudaError_t launch_derive(const tabx_config* cfgs, DerivedCfg* dcfgs, int k0, int k1,
+                          cudaStream_t stream);
 cudaError_t launch_export(const DevState& st, const tabx_state& d, int64_t B, int N, int W,
                           int sm_count, cudaStream_t stream);
-cudaError_t launch_import(const DevState& st, const tabx_state& s, int64_t B, int N, int W,
-                          int sm_count, cudaStream_t stream);
+cudaError_t launch_import(const DevState& st, const tabx_state& s, const tabx_config* cfgs,
+                          const DerivedCfg* dcfgs, int64_t B, int N, int W, int sm_count,
+                          cudaStream_t stream);
 cudaError_t launch_stats(const DevState& st, int64_t B, double* out, int reset,
                          cudaStream_t stream);
 cudaError_t launch_sincos_debug(const double* x, double* s, double* c, int64_t n,
@@ -37,6 +41,7 @@ struct tabx_handle {
   bool any_external = false;
   std::vector<tabx_config> cfg_host;
   tabx_config* cfg_dev = nullptr;
+  DerivedCfg* dcfg_dev = nullptr;
   DevState st{};
   void* arena = nullptr;
   Sync* sync = nullptr;
@@ -86,6 +91,7 @@ static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
   Params P;
   P.st = h->st;
   P.cfgs = h->cfg_dev;
+  P.dcfgs = h->dcfg_dev;
   P.sync = h->sync;
   P.actions = actions;
   if (out) {
@@ -135,6 +141,7 @@ static int find_or_add_config(tabx_handle* h, const tabx_config* c, int32_t* idx
   TABX_CUDA(cudaMemcpyAsync(h->cfg_dev + k, c, sizeof(tabx_config), cudaMemcpyHostToDevice,
                             h->stream),
             "config upload");
+  TABX_CUDA(launch_derive(h->cfg_dev, h->dcfg_dev, (int)k, (int)k + 1, h->stream), "derive");
   if (c->controller[0] == TABX_CTRL_EXTERNAL || c->controller[1] == TABX_CTRL_EXTERNAL)
     h->any_external = true;
   *idx = (int32_t)k;
@@ -193,7 +200,8 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
          o_ret = take(8 * B), o_flags = take(B), o_win = take(B), o_rea = take(B),
          o_fk = take(B), o_cfg = take(4 * B), o_pos = take(16 * U), o_hd = take(8 * U),
          o_vel = take(16 * U), o_imp = take(16 * U), o_hp = take(8 * U), o_cd = take(8 * U),
-         o_rv = take(8 * U), o_mem = take(16 * U), o_ub = take(U), o_vis = take(4 * U * W),
+         o_rv = take(8 * U), o_mem = take(16 * U), o_hcs = take(16 * U), o_zb = take(4 * U),
+         o_ub = take(U), o_vis = take(4 * U * W),
          o_atk = take(4 * U * W), o_se = take(4 * B), o_sw = take(4 * B), o_sf = take(4 * B),
          o_stie = take(4 * B), o_sel = take(4 * B), o_sl = take(8 * B), o_sr = take(8 * B),
          o_sync = take(sizeof(Sync)), o_stats = take(8 * TABX_NUM_STATS);
@@ -203,7 +211,10 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
     return cuda_fail(e, "state allocation");
   }
   e = cudaMalloc((void**)&h->cfg_dev, sizeof(tabx_config) * TABX_MAX_CONFIGS);
+  if (e == cudaSuccess)
+    e = cudaMalloc((void**)&h->dcfg_dev, sizeof(DerivedCfg) * TABX_MAX_CONFIGS);
   if (e != cudaSuccess) {
+    cudaFree(h->cfg_dev);
     cudaFree(h->arena);
     delete h;
     return cuda_fail(e, "config table allocation");
@@ -228,6 +239,8 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   st.cooldown = (double*)(a + o_cd);
   st.reveal = (double*)(a + o_rv);
   st.mem_pos = (double2*)(a + o_mem);
+  st.hcs = (double2*)(a + o_hcs);
+  st.zbits = (uint32_t*)(a + o_zb);
   st.ubits = (uint8_t*)(a + o_ub);
   st.vis = (uint32_t*)(a + o_vis);
   st.atk = (uint32_t*)(a + o_atk);
@@ -250,16 +263,19 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   }
   e = cudaMemcpyAsync(h->cfg_dev, configs, sizeof(tabx_config) * n_configs,
                       cudaMemcpyHostToDevice, h->stream);
+  if (e == cudaSuccess) e = launch_derive(h->cfg_dev, h->dcfg_dev, 0, n_configs, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(h->arena, 0, off, h->stream);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(st.seed, seeds, 8 * B, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess && env_config)
     e = cudaMemcpyAsync(st.cfg, env_config, 4 * B, cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = cudaMemsetAsync(&h->sync->err_index, 0xFF, 8, h->stream);
-  if (e == cudaSuccess) e = launch_spawn(st, h->cfg_dev, 0, B, N, (int)W, 1, h->sm_count, h->stream);
+  if (e == cudaSuccess)
+    e = launch_spawn(st, h->cfg_dev, h->dcfg_dev, 0, B, N, (int)W, 1, h->sm_count, h->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // host arrays may be freed
   if (e != cudaSuccess) {
     rc = cuda_fail(e, "tabx_create");
+    cudaFree(h->dcfg_dev);
     cudaFree(h->cfg_dev);
     cudaFree(h->arena);
     delete h;
@@ -273,6 +289,7 @@ int tabx_destroy(tabx_handle* h) {
   if (!h) return TABX_OK;
   DeviceGuard guard(h->device);
   cudaStreamSynchronize(h->stream);
+  cudaFree(h->dcfg_dev);
   cudaFree(h->cfg_dev);
   cudaFree(h->arena);
   delete h;
@@ -344,7 +361,8 @@ int tabx_reset_env(tabx_handle* h, int64_t b, const tabx_config* config, uint64_
               "seed upload");
     TABX_CUDA(cudaStreamSynchronize(h->stream), "reset_env sync");
   }
-  TABX_CUDA(launch_spawn(h->st, h->cfg_dev, b, b + 1, h->N, h->W, 0, h->sm_count, h->stream),
+  TABX_CUDA(launch_spawn(h->st, h->cfg_dev, h->dcfg_dev, b, b + 1, h->N, h->W, 0, h->sm_count,
+                         h->stream),
             "spawn launch");
   return tabx_init_output(h, out);
 }
@@ -366,7 +384,8 @@ int tabx_respawn_all(tabx_handle* h, const uint64_t* seeds, const int32_t* env_c
     TABX_CUDA(cudaMemsetAsync(h->st.cfg, 0, 4 * h->B, h->stream), "env config");
   }
   TABX_CUDA(cudaMemsetAsync(&h->sync->err_index, 0xFF, 8, h->stream), "error clear");
-  TABX_CUDA(launch_spawn(h->st, h->cfg_dev, 0, h->B, h->N, h->W, 1, h->sm_count, h->stream),
+  TABX_CUDA(launch_spawn(h->st, h->cfg_dev, h->dcfg_dev, 0, h->B, h->N, h->W, 1, h->sm_count,
+                         h->stream),
             "spawn launch");
   TABX_CUDA(cudaStreamSynchronize(h->stream), "respawn sync");
   return TABX_OK;
@@ -385,7 +404,9 @@ int tabx_export_state(tabx_handle* h, const tabx_state* dst) {
 int tabx_import_state(tabx_handle* h, const tabx_state* src) {
   if (!h || !src) return fail(TABX_E_ARGUMENT, "tabx_import_state: bad argument");
   DeviceGuard guard(h->device);
-  TABX_CUDA(launch_import(h->st, *src, h->B, h->N, h->W, h->sm_count, h->stream), "import");
+  TABX_CUDA(launch_import(h->st, *src, h->cfg_dev, h->dcfg_dev, h->B, h->N, h->W, h->sm_count,
+                          h->stream),
+            "import");
   TABX_CUDA(cudaMemsetAsync(h->sync->refresh, 0, sizeof(h->sync->refresh), h->stream),
             "refresh clear");
   return TABX_OK;

@@ -44,6 +44,8 @@ struct DevState {
   double* cooldown;
   double* reveal;
   double2* mem_pos;
+  double2* hcs;      // cached (cos, sin) of heading, libm-exact
+  uint32_t* zbits;   // zone-membership bits at the current position
   uint8_t* ubits;
   uint32_t* vis;
   uint32_t* atk;
@@ -67,11 +69,23 @@ struct Sync {
   int32_t pad;
 };
 
+// Per-config values derived once on the device (not part of the ABI):
+// reciprocals for the fast exact-rounding paths, float copies for filters.
+struct DerivedCfg {
+  double rw, rh;                      // 1/field_w, 1/field_h
+  double rax[TABX_MAX_ZONES], ray[TABX_MAX_ZONES];
+  double rmh[TABX_MAX_UNITS];         // 1/max_health
+  double rucd[TABX_MAX_UNITS];        // 1/cooldown (0 if cooldown == 0)
+  uint32_t lava_m, bush_m, swamp_m;   // zone-type bit masks
+  int32_t n_ally, n_enemy;            // team roster sizes (active units)
+};
+
 enum Mode : int { MODE_STEP = 0, MODE_INIT = 1, MODE_REFRESH = 2 };
 
 struct Params {
   DevState st;
   const tabx_config* cfgs;
+  const DerivedCfg* dcfgs;
   Sync* sync;
   const int64_t* actions;  // [B*N] or nullptr
   tabx_outputs out;
@@ -82,5 +96,34 @@ struct Params {
   int stage_rows;    // observation rows per staged chunk
   int stage_floats;  // floats per stage buffer (multiple of 4)
 };
+
+// Zone membership bits at (x, y) (arrays.py:329-335).  The reference
+// divides by the semi-axes; here the quotients are first estimated with the
+// precomputed reciprocals (error < 3 ulp) and the exact division is redone
+// only when the ellipse sum lands within 1e-9 of 1.
+__device__ __forceinline__ uint32_t zone_bits(const tabx_config* __restrict__ C,
+                                              const DerivedCfg* __restrict__ DC, int Z, double x,
+                                              double y) {
+  uint32_t bits = 0;
+  for (int z = 0; z < Z; ++z) {
+    if (C->zone_type[z] == TABX_ZONE_NONE) continue;
+    const double ex = x - C->zone_cx[z];
+    const double ey = y - C->zone_cy[z];
+    const double ax = ex * DC->rax[z], ay = ey * DC->ray[z];
+    const double s = ax * ax + ay * ay;
+    bool in;
+    if (s < 1.0 - 1e-9) {
+      in = true;
+    } else if (s > 1.0 + 1e-9) {
+      in = false;
+    } else {
+      const double qx = ex / C->zone_ax[z];
+      const double qy = ey / C->zone_ay[z];
+      in = qx * qx + qy * qy <= 1.0;
+    }
+    if (in) bits |= 1u << z;
+  }
+  return bits;
+}
 
 }  // namespace tabx

@@ -109,25 +109,16 @@ __device__ __forceinline__ bool bit_of(const uint32_t* row, int j) {
   return (row[j >> 5] >> (j & 31)) & 1u;
 }
 
-// Zone membership bits at (x, y) (arrays.py:329-335).
-__device__ __forceinline__ uint32_t zone_bits(const tabx_config* __restrict__ C, int Z, double x,
-                                              double y) {
-  uint32_t bits = 0;
-  for (int z = 0; z < Z; ++z) {
-    if (C->zone_type[z] == TABX_ZONE_NONE) continue;
-    double qx = (x - C->zone_cx[z]) / C->zone_ax[z];
-    double qy = (y - C->zone_cy[z]) / C->zone_ay[z];
-    if (qx * qx + qy * qy <= 1.0) bits |= 1u << z;
-  }
-  return bits;
-}
-
-__device__ __forceinline__ uint32_t zone_type_mask(const tabx_config* __restrict__ C, int Z,
-                                                   int type) {
-  uint32_t m = 0;
-  for (int z = 0; z < Z; ++z)
-    if (C->zone_type[z] == type) m |= 1u << z;
-  return m;
+// float32(fl64(x / y)) without the float64 division: q = x * fl(1/y) is
+// within 3 ulp of fl64(x / y), so both round to the same float32 unless q
+// sits within a few ulp of a float32 rounding midpoint (low 29 mantissa bits
+// near 0x10000000) -- then, and for float32-subnormal magnitudes, divide.
+__device__ __forceinline__ float f32_quot(double x, double y, double ry) {
+  double q = x * ry;
+  const int dlt = (int)((uint32_t)__double2loint(q) & 0x1FFFFFFFu) - 0x10000000;
+  const double aq = fabs(q);
+  if ((dlt <= 8 && dlt >= -8) || (aq < 2.4e-38 && aq != 0.0) || aq > 1e37) q = x / y;
+  return __double2float_rn(q);
 }
 
 // effective_speed multiplier: sequential product over zones (arrays.py:338-343)
@@ -224,24 +215,43 @@ __device__ __forceinline__ UnitStatic load_static(const tabx_config* __restrict_
   return u;
 }
 
+// sqrt(a2) < sqrt(b2) for the correctly rounded float64 sqrt, deciding on
+// the squares unless they are within 1e-14 (where the roots may round equal).
+__device__ __forceinline__ bool closer(double a2, double b2) {
+  if (!(a2 < b2)) return false;
+  if (a2 < b2 * (1.0 - 1e-14)) return true;
+  return sqrt(a2) < sqrt(b2);
+}
+
 // Visibility / attackable rows of observer i and its nearest attackable
-// target (perception.py:52-96, combat.py:16-83).  Reads positions, headings,
-// reveal timers, flags and zone bits of every unit from shared memory and
-// writes the two N-bit rows to S.vis / S.atk; returns the target or -1.
+// target (perception.py:52-96, combat.py:16-83).  Writes the two N-bit rows
+// to S.vis / S.atk and returns the target or -1.
+//
+// Each pair is first classified in float32 (range against sight_range^2,
+// view wedge via rsqrt, strike box) with margins two orders of magnitude
+// above the float32 error bound; only pairs inside a margin (and the few
+// attackable pairs, whose exact distance orders the target choice) are
+// evaluated with the reference's float64 expressions.  The verdicts are
+// therefore exactly the float64 ones.
 template <int W>
-__device__ __noinline__ int cache_row(EnvSmem<W>& S, int i, int N, double cos_half,
-                                      double srange, double dmg, double reach, double rad,
-                                      uint32_t bush_m) {
+__device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, double cos_half,
+                                              double srange, double dmg, double reach, double rad,
+                                              uint32_t bush_m) {
   uint32_t vis[W], atk[W];
 #pragma unroll
   for (int k = 0; k < W; ++k) vis[k] = atk[k] = 0u;
   int tgt = -1;
   const uint32_t uf_i = S.uf[i];
-  const bool act_i = (uf_i & UF_ACTIVE) != 0;
-  if (act_i) {  // vis requires both active; atk requires vis
+  if (uf_i & UF_ACTIVE) {  // vis requires both active; atk requires vis
     const double px = S.px[i], py = S.py[i], ch = S.ch[i], sh = S.sh[i];
-    const bool live_i = (uf_i & UF_ALIVE) != 0;
+    const float chf = (float)ch, shf = (float)sh;
+    const float sr2 = (float)(srange * srange);
+    const float sr2_lo = sr2 * 0.99999f, sr2_hi = sr2 * 1.00001f;
+    const float cf = (float)cos_half;
+    const float cf_lo = cf - 2e-5f, cf_hi = cf + 2e-5f;
+    const float reachf = (float)reach, radf = (float)rad;
     const bool enemy_i = (uf_i & UF_ENEMY) != 0;
+    const bool can_hit = (uf_i & UF_ALIVE) && dmg != 0.0;
     const uint32_t bush_i = S.zin[i] & bush_m;
     double best = 0.0;
     for (int j = 0; j < N; ++j) {
@@ -249,29 +259,63 @@ __device__ __noinline__ int cache_row(EnvSmem<W>& S, int i, int N, double cos_ha
       if (!(uj & UF_ACTIVE)) continue;
       const double dx = S.px[j] - px;
       const double dy = S.py[j] - py;
-      const double dist = sqrt(dx * dx + dy * dy);
-      const double lx = dx * ch + dy * sh;
-      const double cdev = dist > 0.0 ? lx / dist : 1.0;
-      const bool wedge = cdev >= cos_half;
-      if (!(dist <= srange && wedge)) continue;
+      const float dxf = (float)dx, dyf = (float)dy;
+      const float d2f = dxf * dxf + dyf * dyf;
+      if (d2f >= sr2_hi && d2f > 0.0f) continue;  // certainly beyond sight range
+      const float lxf = dxf * chf + dyf * shf;
+      double dist = -1.0;
+      bool seen;
+      bool exact = true;
+      if (d2f > 1e-30f && d2f <= sr2_lo) {
+        const float cdevf = lxf * rsqrtf(d2f);
+        if (cdevf >= cf_hi) {
+          seen = true;
+          exact = false;
+        } else if (cdevf <= cf_lo) {
+          seen = false;
+          exact = false;
+        }
+      }
+      if (exact) {
+        dist = sqrt(dx * dx + dy * dy);
+        const double lx = dx * ch + dy * sh;
+        const double cdev = dist > 0.0 ? lx / dist : 1.0;
+        seen = dist <= srange && cdev >= cos_half;
+      }
+      if (!seen) continue;
       const bool foe = ((uj & UF_ENEMY) != 0) != enemy_i;
       const uint32_t bush_j = S.zin[j] & bush_m;
-      const bool hidden = bush_j != 0u && foe && (bush_i & bush_j) == 0u && S.rv[j] <= 0.0;
-      if (hidden) continue;
+      if (bush_j != 0u && foe && (bush_i & bush_j) == 0u && S.rv[j] <= 0.0) continue;
       vis[j >> 5] |= 1u << (j & 31);
-      const bool role = dmg > 0.0 ? foe : (dmg < 0.0 && !foe);
-      if (!(role && live_i && (uj & UF_ALIVE) && j != i)) continue;
-      const double ly = (-dx) * sh + dy * ch;
-      const double cx = np_clip(lx, 0.0, reach);
-      const double cy = np_clip(ly, -rad, rad);
-      const double gx = lx - cx, gy = ly - cy;
+      const bool role = dmg > 0.0 ? foe : !foe;
+      if (!(can_hit && role && (uj & UF_ALIVE) && j != i)) continue;
       const double rj = S.rad[j];
-      if (gx * gx + gy * gy <= rj * rj) {
-        atk[j >> 5] |= 1u << (j & 31);
-        if (tgt < 0 || dist < best) {
-          best = dist;
-          tgt = j;
-        }
+      const float rjf = (float)rj;
+      const float lyf = (-dxf) * shf + dyf * chf;
+      const float gxf = lxf - fminf(fmaxf(lxf, 0.0f), reachf);
+      const float gyf = lyf - fminf(fmaxf(lyf, -radf), radf);
+      const float gapf = gxf * gxf + gyf * gyf;
+      const float rj2f = rjf * rjf;
+      const float L = fabsf(lxf) + fabsf(lyf) + reachf + radf + rjf;
+      const float mb = 3e-5f * L * L;
+      bool box;
+      if (gapf < rj2f - mb) {
+        box = true;
+      } else if (gapf > rj2f + mb) {
+        box = false;
+      } else {
+        const double lx = dx * ch + dy * sh;
+        const double ly = (-dx) * sh + dy * ch;
+        const double gx = lx - np_clip(lx, 0.0, reach);
+        const double gy = ly - np_clip(ly, -rad, rad);
+        box = gx * gx + gy * gy <= rj * rj;
+      }
+      if (!box) continue;
+      atk[j >> 5] |= 1u << (j & 31);
+      if (dist < 0.0) dist = sqrt(dx * dx + dy * dy);
+      if (tgt < 0 || dist < best) {
+        best = dist;
+        tgt = j;
       }
     }
   }
@@ -284,9 +328,24 @@ __device__ __noinline__ int cache_row(EnvSmem<W>& S, int i, int N, double cos_ha
 }
 
 template <int W>
+__device__ __noinline__ int cache_row_call(EnvSmem<W>& S, int i, int N, double cos_half,
+                                           double srange, double dmg, double reach, double rad,
+                                           uint32_t bush_m) {
+  return cache_row_body<W>(S, i, N, cos_half, srange, dmg, reach, rad, bush_m);
+}
+
+// Out-of-line variant for the rare call sites (refresh, init, auto-reset).
+template <int W>
 __device__ __forceinline__ int cache_row_of(EnvSmem<W>& S, int i, int N, const UnitStatic& U,
                                             uint32_t bush_m) {
-  return cache_row<W>(S, i, N, U.cos_half, U.srange, U.dmg, U.range, U.rad, bush_m);
+  return cache_row_call<W>(S, i, N, U.cos_half, U.srange, U.dmg, U.range, U.rad, bush_m);
+}
+
+// Inline variant for the every-step call (stage 8).
+template <int W>
+__device__ __forceinline__ int cache_row_inl(EnvSmem<W>& S, int i, int N, const UnitStatic& U,
+                                             uint32_t bush_m) {
+  return cache_row_body<W>(S, i, N, U.cos_half, U.srange, U.dmg, U.range, U.rad, bush_m);
 }
 
 // ------------------------------------------------ observation streaming --
@@ -344,9 +403,10 @@ template <int W>
 __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* __restrict__ glob,
                                                int64_t b, int N, int Z, int D, int G, int R,
                                                int SF, EnvSmem<W>& S, float* stage,
-                                               const tabx_config* __restrict__ C, int tid) {
+                                               const tabx_config* __restrict__ C,
+                                               const DerivedCfg* __restrict__ DC, int tid) {
   constexpr int NT = 32 * W;
-  const double fw = C->field_w, fh = C->field_h;
+  const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
   const int M = N - 1;
   const int zoff = TABX_OWN_DIM + TABX_OTHER_DIM * M;
   int buf = 0;
@@ -375,8 +435,8 @@ __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* _
             const float* oj = S.own[j];
             blk[0] = oj[0];
             blk[1] = oj[1];
-            blk[2] = __double2float_rn((S.px[j] - S.px[r]) / fw);
-            blk[3] = __double2float_rn((S.py[j] - S.py[r]) / fh);
+            blk[2] = f32_quot(S.px[j] - S.px[r], fw, rw);
+            blk[3] = f32_quot(S.py[j] - S.py[r], fh, rh);
 #pragma unroll
             for (int f = 4; f < TABX_OWN_DIM; ++f) blk[f] = oj[f];
             blk[15] = (uj & UF_ENEMY) ? 1.0f : 0.0f;
@@ -402,8 +462,8 @@ __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* _
           blk[0] = ty == 1 ? 1.0f : 0.0f;
           blk[1] = ty == 2 ? 1.0f : 0.0f;
           blk[2] = ty == 3 ? 1.0f : 0.0f;
-          blk[3] = __double2float_rn((C->zone_cx[z] - S.px[r]) / fw);
-          blk[4] = __double2float_rn((C->zone_cy[z] - S.py[r]) / fh);
+          blk[3] = f32_quot(C->zone_cx[z] - S.px[r], fw, rw);
+          blk[4] = f32_quot(C->zone_cy[z] - S.py[r], fh, rh);
           blk[5] = __double2float_rn(C->zone_ax[z]);
           blk[6] = __double2float_rn(C->zone_ay[z]);
           blk[7] = __double2float_rn(C->zone_effect[z]);
@@ -435,8 +495,8 @@ __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* _
       } else {
         switch (f) {
           case 0: case 1: case 2: v = ty == f + 1 ? 1.0f : 0.0f; break;
-          case 3: v = __double2float_rn(C->zone_cx[z] / fw); break;
-          case 4: v = __double2float_rn(C->zone_cy[z] / fh); break;
+          case 3: v = f32_quot(C->zone_cx[z], fw, rw); break;
+          case 4: v = f32_quot(C->zone_cy[z], fh, rh); break;
           case 5: v = __double2float_rn(C->zone_ax[z]); break;
           case 6: v = __double2float_rn(C->zone_ay[z]); break;
           default: v = __double2float_rn(C->zone_effect[z]); break;
@@ -453,24 +513,25 @@ __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* _
 }
 
 // Own-feature block of unit i (perception.py:108-132) rounded to float32.
-__device__ __forceinline__ void own_features(float* o, const UnitStatic& U, double hp, double px,
-                                             double py, double ch, double sh, double cd,
-                                             bool alive, double fw, double fh) {
+__device__ __forceinline__ void own_features(float* o, const UnitStatic& U, double rmh,
+                                             double rucd, double hp, double px, double py,
+                                             double ch, double sh, double cd, bool alive,
+                                             double fw, double fh, double rw, double rh) {
   if (!U.active) {
 #pragma unroll
     for (int f = 0; f < TABX_OWN_DIM; ++f) o[f] = 0.0f;
     return;
   }
-  o[0] = __double2float_rn(hp / U.mh);
-  o[1] = __double2float_rn(U.mh / 1000.0);
-  o[2] = __double2float_rn(px / fw);
-  o[3] = __double2float_rn(py / fh);
+  o[0] = f32_quot(hp, U.mh, rmh);
+  o[1] = f32_quot(U.mh, 1000.0, 0.001);
+  o[2] = f32_quot(px, fw, rw);
+  o[3] = f32_quot(py, fh, rh);
   o[4] = __double2float_rn(ch);
   o[5] = __double2float_rn(sh);
   o[6] = __double2float_rn(U.range);
   o[7] = __double2float_rn(U.dmg);
   o[8] = __double2float_rn(cd);
-  o[9] = U.ucd > 0.0 ? __double2float_rn(cd / U.ucd) : 0.0f;
+  o[9] = U.ucd > 0.0 ? f32_quot(cd, U.ucd, rucd) : 0.0f;
   o[10] = __double2float_rn(U.rad);
   o[11] = __double2float_rn(U.mass);
   o[12] = __double2float_rn(U.sangle);
@@ -509,6 +570,7 @@ __device__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restric
                                double xi, uint32_t bush_m, double& mx, double& my, bool& memv) {
   const double px = S.px[i], py = S.py[i];
   // target candidates: visible, alive & active, not self
+  // squared distances; closer() orders them exactly as their float64 roots
   double bf = 0.0, bi = 0.0, bn = 0.0, bm = 0.0, bmd = 0.0;
   int tf = -1, ti = -1, tn = -1, tm = -1;
   for (int j = 0; j < N; ++j) {
@@ -516,15 +578,15 @@ __device__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restric
     if (j == i || !bit_of(vis, j) || (uj & (UF_ACTIVE | UF_ALIVE)) != (UF_ACTIVE | UF_ALIVE))
       continue;
     const double dx = S.px[j] - px, dy = S.py[j] - py;
-    const double d = sqrt(dx * dx + dy * dy);
+    const double d = dx * dx + dy * dy;
     const bool foe = ((uj & UF_ENEMY) != 0) != U.enemy;
     if (!foe) {
-      if (tf < 0 || d < bf) { bf = d; tf = j; }
-      if ((uj & UF_INJURED) && (ti < 0 || d < bi)) { bi = d; ti = j; }
+      if (tf < 0 || closer(d, bf)) { bf = d; tf = j; }
+      if ((uj & UF_INJURED) && (ti < 0 || closer(d, bi))) { bi = d; ti = j; }
     } else {
-      if (tn < 0 || d < bn) { bn = d; tn = j; }
+      if (tn < 0 || closer(d, bn)) { bn = d; tn = j; }
       const double m = S.mh[j];
-      if (tm < 0 || m < bm || (m == bm && d < bmd)) { bm = m; bmd = d; tm = j; }
+      if (tm < 0 || m < bm || (m == bm && closer(d, bmd))) { bm = m; bmd = d; tm = j; }
     }
   }
   int tgt;
@@ -563,7 +625,7 @@ __device__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restric
     const double cdev = dist > 0.0 ? lx / dist : 1.0;
     if (box && cdev >= U.cos_half) act = A_ROTATE;
   }
-  if (act < 0 && U.ranger && has_near && bn < xi * U.range)
+  if (act < 0 && U.ranger && has_near && sqrt(bn) < xi * U.range)
     act = best_move(px, py, S.px[tn], S.py[tn], step, true);
   if (act < 0 && has) {
     const double touch = U.rad + tr + 0.5;
@@ -612,11 +674,11 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const int64_t u = b * N + i;
   const DevState& st = P.st;
   const tabx_config* __restrict__ C = P.cfgs + st.cfg[b];
+  const DerivedCfg* __restrict__ DC = P.dcfgs + st.cfg[b];
   const UnitStatic U = load_static(C, i, valid);
-  const uint32_t bush_m = zone_type_mask(C, Z, TABX_ZONE_BUSH);
-  const uint32_t lava_m = zone_type_mask(C, Z, TABX_ZONE_LAVA);
-  const uint32_t swamp_m = zone_type_mask(C, Z, TABX_ZONE_SWAMP);
-  const double dt = C->dt, fw = C->field_w, fh = C->field_h;
+  const uint32_t bush_m = DC->bush_m, lava_m = DC->lava_m, swamp_m = DC->swamp_m;
+  const double dt = C->dt, fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
+  const double rmh = valid ? DC->rmh[i] : 1.0, rucd = valid ? DC->rucd[i] : 0.0;
 
   // ---- lane + unit state
   uint8_t lf = st.flags[b];
@@ -629,6 +691,8 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 
   double px = 0.0, py = 0.0, hd = 0.0, hp = 0.0, cd = 0.0, rv = 0.0;
   double ivx = 0.0, ivy = 0.0, vlx = 0.0, vly = 0.0, mx = 0.0, my = 0.0;
+  double ch = 1.0, sh = 0.0;  // libm cos/sin of hd, cached in the state
+  uint32_t zin = 0u;          // zone bits at (px, py), cached in the state
   bool alive = false, memv = false;
   if (valid) {
     const double2 p = st.pos[u];
@@ -650,8 +714,11 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     const uint8_t ub = st.ubits[u];
     alive = ub & U_ALIVE;
     memv = ub & U_MEMV;
+    const double2 cs = st.hcs[u];
+    ch = cs.x;
+    sh = cs.y;
+    zin = st.zbits[u];
   }
-  double ch = libm_cos(hd), sh = libm_sin(hd);
 
   auto publish = [&](void) {
     S.px[i] = px;
@@ -664,11 +731,10 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     S.dmg[i] = U.dmg;
     S.uf[i] = (U.active ? UF_ACTIVE : 0u) | (alive ? UF_ALIVE : 0u) | (U.enemy ? UF_ENEMY : 0u) |
               (U.kin ? UF_KIN : 0u) | (hp < U.mh ? UF_INJURED : 0u);
-    S.zin[i] = valid ? zone_bits(C, Z, px, py) : 0u;
+    S.zin[i] = zin;
   };
 
-  const int n_ally = env_count<W>(valid && U.active && !U.enemy, S, i);
-  const int n_enemy = env_count<W>(valid && U.active && U.enemy, S, i);
+  const int n_ally = DC->n_ally, n_enemy = DC->n_enemy;
 
   uint32_t vis[W], atk[W];
   int tgt = -1;
@@ -699,11 +765,11 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     double ra, re;
     team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
     prev_gap = ra - re;
-    own_features(S.own[i], U, hp, px, py, ch, sh, cd, alive, fw, fh);
+    own_features(S.own[i], U, rmh, rucd, hp, px, py, ch, sh, cd, alive, fw, fh, rw, rh);
     env_sync<W>();
     const tabx_outputs& O = P.out;
     emit_observations<W>(O.observations, O.global_state, b, N, Z, P.D, P.G, P.stage_rows,
-                         P.stage_floats, S, stage, C, i);
+                         P.stage_floats, S, stage, C, DC, i);
     if (valid) {
       const bool ctl = alive && U.active;
       if (O.action_mask) {
@@ -815,10 +881,22 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     for (int j = i + 1; j < N; ++j) {
       if (!(S.uf[j] & UF_ACTIVE)) continue;
       const double dx = S.px[j] - px, dy = S.py[j] - py;
-      const double dist = sqrt(dx * dx + dy * dy);
       const double rs = U.rad + S.rad[j];
-      const double depth = dist == 0.0 ? rs : rs - dist;
-      if (depth > 0.0) {
+      // float32 filter on squared distance vs rs^2 (margin 1e-5 relative);
+      // near-contact pairs get the reference's float64 depth test
+      const float dxf = (float)dx, dyf = (float)dy;
+      const float d2f = dxf * dxf + dyf * dyf;
+      const float rs2f = (float)(rs * rs);
+      if (d2f > rs2f * 1.00001f) continue;
+      bool hit;
+      if (d2f < rs2f * 0.99999f && d2f > 1e-30f) {
+        hit = true;
+      } else {
+        const double dist = sqrt(dx * dx + dy * dy);
+        const double depth = dist == 0.0 ? rs : rs - dist;
+        hit = depth > 0.0;
+      }
+      if (hit) {
         trow[j >> 5] |= 1u << (j & 31);
         any_touch = true;
       }
@@ -896,10 +974,11 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   }
 
   // 8. caches at the post-move state (environment.py:254-257)
+  zin = valid ? zone_bits(C, DC, Z, px, py) : 0u;
   env_sync<W>();
   publish();
   env_sync<W>();
-  tgt = cache_row_of<W>(S, i, N, U, bush_m);
+  tgt = cache_row_inl<W>(S, i, N, U, bush_m);
 #pragma unroll
   for (int k = 0; k < W; ++k) {
     vis[k] = S.vis[i * W + k];
@@ -976,14 +1055,14 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   // ---- outputs of this step (observation uses stage-8 caches, post-step state)
   const tabx_outputs& O = P.out;
   const bool resets = P.auto_reset && (lf & F_DONE);
-  own_features(S.own[i], U, hp, px, py, ch, sh, cd, alive, fw, fh);
+  own_features(S.own[i], U, rmh, rucd, hp, px, py, ch, sh, cd, alive, fw, fh, rw, rh);
   S.uf[i] = (S.uf[i] & ~UF_ALIVE) | (alive ? UF_ALIVE : 0u);
   env_sync<W>();
   {
     float* ob = resets ? O.final_observations : O.observations;
     float* gb = resets ? O.final_global_state : O.global_state;
     emit_observations<W>(ob, gb, b, N, Z, P.D, P.G, P.stage_rows, P.stage_floats, S, stage, C,
-                         i);
+                         DC, i);
   }
   if (valid) {
     if (O.rewards) O.rewards[u] = (float)reward_i;
@@ -1046,6 +1125,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     fk = -1;
     ch = libm_cos(hd);
     sh = libm_sin(hd);
+    zin = valid ? zone_bits(C, DC, Z, px, py) : 0u;
     publish();
     env_sync<W>();
     cache_row_of<W>(S, i, N, U, bush_m);
@@ -1056,10 +1136,10 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     }
     team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
     prev_gap = ra - re;
-    own_features(S.own[i], U, hp, px, py, ch, sh, cd, alive, fw, fh);
+    own_features(S.own[i], U, rmh, rucd, hp, px, py, ch, sh, cd, alive, fw, fh, rw, rh);
     env_sync<W>();
     emit_observations<W>(O.observations, O.global_state, b, N, Z, P.D, P.G, P.stage_rows,
-                         P.stage_floats, S, stage, C, i);
+                         P.stage_floats, S, stage, C, DC, i);
     if (valid && O.action_mask) {
       const bool c2 = alive && U.active;
       uint8_t* m = O.action_mask + u * TABX_NUM_ACTIONS;
@@ -1084,6 +1164,8 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     st.cooldown[u] = cd;
     st.reveal[u] = rv;
     st.mem_pos[u] = make_double2(mx, my);
+    st.hcs[u] = make_double2(ch, sh);
+    st.zbits[u] = zin;
     st.ubits[u] = (alive ? U_ALIVE : 0) | (memv ? U_MEMV : 0);
 #pragma unroll
     for (int k = 0; k < W; ++k) {
