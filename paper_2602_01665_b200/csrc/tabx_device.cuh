@@ -97,6 +97,12 @@ struct Params {
   int stage_floats;  // floats per stage buffer (multiple of 4)
 };
 
+__device__ __noinline__ static bool zone_exact(double ex, double ey, double ax, double ay) {
+  const double qx = ex / ax;
+  const double qy = ey / ay;
+  return qx * qx + qy * qy <= 1.0;
+}
+
 // Zone membership bits at (x, y) (arrays.py:329-335).  The reference
 // divides by the semi-axes; here the quotients are first estimated with the
 // precomputed reciprocals (error < 3 ulp) and the exact division is redone
@@ -117,9 +123,7 @@ __device__ __forceinline__ uint32_t zone_bits(const tabx_config* __restrict__ C,
     } else if (s > 1.0 + 1e-9) {
       in = false;
     } else {
-      const double qx = ex / C->zone_ax[z];
-      const double qy = ey / C->zone_ay[z];
-      in = qx * qx + qy * qy <= 1.0;
+      in = zone_exact(ex, ey, C->zone_ax[z], C->zone_ay[z]);
     }
     if (in) bits |= 1u << z;
   }

@@ -113,11 +113,17 @@ __device__ __forceinline__ bool bit_of(const uint32_t* row, int j) {
 // within 3 ulp of fl64(x / y), so both round to the same float32 unless q
 // sits within a few ulp of a float32 rounding midpoint (low 29 mantissa bits
 // near 0x10000000) -- then, and for float32-subnormal magnitudes, divide.
+// Rare exact fallbacks live out of line: a call cannot be speculated, so the
+// float64 division / square-root sequences only run on the lanes that need
+// them instead of being if-converted into every warp's path.
+__device__ __noinline__ double slow_div(double x, double y) { return x / y; }
+__device__ __noinline__ double slow_sqrt(double x) { return sqrt(x); }
+
 __device__ __forceinline__ float f32_quot(double x, double y, double ry) {
   double q = x * ry;
   const int dlt = (int)((uint32_t)__double2loint(q) & 0x1FFFFFFFu) - 0x10000000;
   const double aq = fabs(q);
-  if ((dlt <= 8 && dlt >= -8) || (aq < 2.4e-38 && aq != 0.0) || aq > 1e37) q = x / y;
+  if ((dlt <= 8 && dlt >= -8) || (aq < 2.4e-38 && aq != 0.0) || aq > 1e37) q = slow_div(x, y);
   return __double2float_rn(q);
 }
 
@@ -220,7 +226,33 @@ __device__ __forceinline__ UnitStatic load_static(const tabx_config* __restrict_
 __device__ __forceinline__ bool closer(double a2, double b2) {
   if (!(a2 < b2)) return false;
   if (a2 < b2 * (1.0 - 1e-14)) return true;
-  return sqrt(a2) < sqrt(b2);
+  return slow_sqrt(a2) < slow_sqrt(b2);
+}
+
+struct Seen {
+  double dist;
+  bool seen;
+};
+
+// Reference float64 verdict of the view wedge + range test (perception.py:52-66).
+__device__ __noinline__ Seen exact_seen(double dx, double dy, double ch, double sh, double srange,
+                                        double cos_half) {
+  Seen r;
+  r.dist = sqrt(dx * dx + dy * dy);
+  const double lx = dx * ch + dy * sh;
+  const double cdev = r.dist > 0.0 ? lx / r.dist : 1.0;
+  r.seen = r.dist <= srange && cdev >= cos_half;
+  return r;
+}
+
+// Reference float64 strike-box test (combat.py:30-40).
+__device__ __noinline__ bool exact_box(double dx, double dy, double ch, double sh, double reach,
+                                       double rad, double rj) {
+  const double lx = dx * ch + dy * sh;
+  const double ly = (-dx) * sh + dy * ch;
+  const double gx = lx - np_clip(lx, 0.0, reach);
+  const double gy = ly - np_clip(ly, -rad, rad);
+  return gx * gx + gy * gy <= rj * rj;
 }
 
 // Visibility / attackable rows of observer i and its nearest attackable
@@ -254,9 +286,11 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
     const bool can_hit = (uf_i & UF_ALIVE) && dmg != 0.0;
     const uint32_t bush_i = S.zin[i] & bush_m;
     double best = 0.0;
+    // the diagonal: distance 0, cos_dev 1 -> visible, never attackable
+    vis[i >> 5] |= 1u << (i & 31);
     for (int j = 0; j < N; ++j) {
       const uint32_t uj = S.uf[j];
-      if (!(uj & UF_ACTIVE)) continue;
+      if (!(uj & UF_ACTIVE) || j == i) continue;
       const double dx = S.px[j] - px;
       const double dy = S.py[j] - py;
       const float dxf = (float)dx, dyf = (float)dy;
@@ -277,10 +311,9 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
         }
       }
       if (exact) {
-        dist = sqrt(dx * dx + dy * dy);
-        const double lx = dx * ch + dy * sh;
-        const double cdev = dist > 0.0 ? lx / dist : 1.0;
-        seen = dist <= srange && cdev >= cos_half;
+        const Seen e = exact_seen(dx, dy, ch, sh, srange, cos_half);
+        dist = e.dist;
+        seen = e.seen;
       }
       if (!seen) continue;
       const bool foe = ((uj & UF_ENEMY) != 0) != enemy_i;
@@ -288,7 +321,7 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
       if (bush_j != 0u && foe && (bush_i & bush_j) == 0u && S.rv[j] <= 0.0) continue;
       vis[j >> 5] |= 1u << (j & 31);
       const bool role = dmg > 0.0 ? foe : !foe;
-      if (!(can_hit && role && (uj & UF_ALIVE) && j != i)) continue;
+      if (!(can_hit && role && (uj & UF_ALIVE))) continue;
       const double rj = S.rad[j];
       const float rjf = (float)rj;
       const float lyf = (-dxf) * shf + dyf * chf;
@@ -304,15 +337,11 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
       } else if (gapf > rj2f + mb) {
         box = false;
       } else {
-        const double lx = dx * ch + dy * sh;
-        const double ly = (-dx) * sh + dy * ch;
-        const double gx = lx - np_clip(lx, 0.0, reach);
-        const double gy = ly - np_clip(ly, -rad, rad);
-        box = gx * gx + gy * gy <= rj * rj;
+        box = exact_box(dx, dy, ch, sh, reach, rad, rj);
       }
       if (!box) continue;
       atk[j >> 5] |= 1u << (j & 31);
-      if (dist < 0.0) dist = sqrt(dx * dx + dy * dy);
+      if (dist < 0.0) dist = slow_sqrt(dx * dx + dy * dy);
       if (tgt < 0 || dist < best) {
         best = dist;
         tgt = j;
@@ -892,7 +921,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
       if (d2f < rs2f * 0.99999f && d2f > 1e-30f) {
         hit = true;
       } else {
-        const double dist = sqrt(dx * dx + dy * dy);
+        const double dist = slow_sqrt(dx * dx + dy * dy);
         const double depth = dist == 0.0 ? rs : rs - dist;
         hit = depth > 0.0;
       }
