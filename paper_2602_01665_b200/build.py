@@ -49,6 +49,13 @@ def _digest() -> str:
     return h.hexdigest()[:16]
 
 
+def _drop_stale() -> None:
+    """Never leave a library from older sources behind a failed build."""
+    for p in (OUT, OUT + ".stamp"):
+        if os.path.exists(p):
+            os.remove(p)
+
+
 def build(verbose: bool = False, force: bool = False) -> str:
     tag = _digest()
     stamp = OUT + ".stamp"
@@ -78,10 +85,14 @@ def build(verbose: bool = False, force: bool = False) -> str:
         if p.returncode != 0:
             failed.append((unit, out))
     if failed:
+        _drop_stale()
         msg = "\n".join(f"--- {u}\n{o}" for u, o in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
     tmp = OUT + ".tmp"
-    subprocess.check_call([cc, *ARCH, "-shared", "-o", tmp, *objs])
+    link = subprocess.run([cc, *ARCH, "-shared", "-o", tmp, *objs], capture_output=True, text=True)
+    if link.returncode != 0:
+        _drop_stale()
+        raise RuntimeError(f"link failed:\n{link.stdout}{link.stderr}")
     os.replace(tmp, OUT)
     with open(stamp, "w") as fh:
         fh.write(tag + "\n")

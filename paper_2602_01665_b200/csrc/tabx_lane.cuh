@@ -116,8 +116,8 @@ __device__ __forceinline__ bool bit_of(const uint32_t* row, int j) {
 // Rare exact fallbacks live out of line: a call cannot be speculated, so the
 // float64 division / square-root sequences only run on the lanes that need
 // them instead of being if-converted into every warp's path.
-__device__ __noinline__ double slow_div(double x, double y) { return x / y; }
-__device__ __noinline__ double slow_sqrt(double x) { return sqrt(x); }
+static __device__ __noinline__ double slow_div(double x, double y) { return x / y; }
+static __device__ __noinline__ double slow_sqrt(double x) { return sqrt(x); }
 
 __device__ __forceinline__ float f32_quot(double x, double y, double ry) {
   double q = x * ry;
@@ -235,7 +235,7 @@ struct Seen {
 };
 
 // Reference float64 verdict of the view wedge + range test (perception.py:52-66).
-__device__ __noinline__ Seen exact_seen(double dx, double dy, double ch, double sh, double srange,
+static __device__ __noinline__ Seen exact_seen(double dx, double dy, double ch, double sh, double srange,
                                         double cos_half) {
   Seen r;
   r.dist = sqrt(dx * dx + dy * dy);
@@ -246,7 +246,7 @@ __device__ __noinline__ Seen exact_seen(double dx, double dy, double ch, double 
 }
 
 // Reference float64 strike-box test (combat.py:30-40).
-__device__ __noinline__ bool exact_box(double dx, double dy, double ch, double sh, double reach,
+static __device__ __noinline__ bool exact_box(double dx, double dy, double ch, double sh, double reach,
                                        double rad, double rj) {
   const double lx = dx * ch + dy * sh;
   const double ly = (-dx) * sh + dy * ch;
