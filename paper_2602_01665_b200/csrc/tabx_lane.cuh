@@ -1215,7 +1215,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 }
 
 #ifndef TABX_MIN_BLOCKS
-#define TABX_MIN_BLOCKS 1
+#define TABX_MIN_BLOCKS 3
 #endif
 template <int W, int EPB>
 __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
