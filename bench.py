@@ -167,7 +167,7 @@ def run_gpu_arm(args) -> int:
     import torch
     import torch.distributed as dist
 
-    from paper_2602_01665_b200 import bindings
+    from paper_2602_01665_b200 import bindings, shard
     from paper_2602_01665_b200.rng import lane_seeds
     from paper_2602_01665_b200.scenario import builtin_scenario, save_scenario
     from paper_2602_01665_b200.sim import BatchSim
@@ -178,10 +178,7 @@ def run_gpu_arm(args) -> int:
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     total = args.envs or DEFAULT_ENVS[args.scenario]
-    per = total // world
-    first = rank * per
-    if rank == world - 1:
-        per = total - first
+    first, per = shard.shard_range(total, world, rank)
     base = builtin_scenario(SCENARIOS[args.scenario])
     sc = base.scripted()
     N, Z = sc.max_units, sc.max_zones
@@ -220,14 +217,9 @@ def run_gpu_arm(args) -> int:
     elapsed_ms = max_over_ranks(t0.elapsed_time(t1))
     kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     value = total * args.steps / (elapsed_ms / 1000.0)
-    stats = sim.episode_stats()
-    if world > 1:
-        vec = torch.tensor([stats[k] for k in ("episodes", "ally_wins", "first_kill_ally",
-                                               "truncation_ties", "sum_length", "sum_return",
-                                               "eliminations")], dtype=torch.float64, device=dev)
-        dist.all_reduce(vec)  # NCCL over NVLink: the per-window episode-statistics reduction
-        stats = dict(zip(("episodes", "ally_wins", "first_kill_ally", "truncation_ties",
-                          "sum_length", "sum_return", "eliminations"), vec.tolist()))
+    # the one collective: per-window episode statistics, NCCL all-reduce over NVLink
+    stats = shard.reduce_episode_stats(sim.episode_stats(), device=dev)
+    stats["summary"] = shard.summarize(stats)
     sim.close()
     del sim
     torch.cuda.empty_cache()

@@ -1263,13 +1263,21 @@ cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream,
   const int threads = 32 * W * EPB;
   const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
   const size_t smem = env_bytes + (size_t)EPB * 2 * P.stage_floats * sizeof(float);
-  cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lane_kernel<W, EPB>, threads, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
+  // attribute + occupancy are host-side queries; cache them per smem size so a
+  // step costs one launch (and stays capturable in a CUDA graph)
+  static size_t cached_smem = 0;
+  static int cached_per_sm = 0;
+  int per_sm = cached_per_sm;
+  if (smem != cached_smem) {
+    cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lane_kernel<W, EPB>, threads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+    cached_smem = smem;
+    cached_per_sm = per_sm;
+  }
   int64_t need = (P.B + EPB - 1) / EPB;
   int64_t cap = (int64_t)sm_count * per_sm;
   int grid = (int)(need < cap ? need : cap);

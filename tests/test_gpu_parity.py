@@ -260,3 +260,27 @@ def test_determinism_full_size():
         gpu.close()
     for a, b in zip(*runs):
         assert torch.equal(a, b)
+
+
+def test_episode_statistics_match_oracle():
+    """Device per-lane accumulators == statistics summed from oracle outputs."""
+    from paper_2602_01665_b200 import shard
+    name = "duel_expert"
+    case = CASES[name]
+    sc = case_scenario(name)
+    seeds = np.array(case_seeds(case), np.uint64)
+    gpu = BatchSim([sc] * case["batch"], seeds, auto_reset=True, device="cuda:0")
+    ora = orc.OracleBatchSim([sc] * case["batch"], seeds, auto_reset=True)
+    acc = {k: 0.0 for k in shard.STAT_KEYS}
+    for _ in range(case["steps"]):
+        gpu.step(None)
+        o = ora.step(None)
+        acc = shard.add_stats(acc, shard.stats_from_outputs(
+            o["done"], o["winner"], o["reason"], o["first_kill"], o["episode_length"],
+            o["episode_return"]))
+    got = gpu.episode_stats()
+    for k in shard.STAT_KEYS:
+        if k == "sum_return":
+            assert got[k] == pytest.approx(acc[k], rel=1e-12, abs=1e-12)
+        else:
+            assert got[k] == acc[k], k
