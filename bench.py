@@ -136,13 +136,57 @@ def cpu_reference(scenario_key: str, envs: int, steps: int, warmup: int, seed: i
             "n_units": len(sc.units), "numpy": np.__version__}
 
 
+def _ref_worker(job):
+    """One host process: its own oracle BatchSim shard, timed after a barrier."""
+    scenario_key, envs, steps, warmup, first, barrier = job
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import tabx_oracle as orc
+
+    from paper_2602_01665_b200.rng import lane_seeds
+    from paper_2602_01665_b200.scenario import builtin_scenario
+
+    sc = builtin_scenario(SCENARIOS[scenario_key]).scripted()
+    sim = orc.OracleBatchSim([sc] * envs, lane_seeds(0, envs, first), auto_reset=True)
+    for _ in range(warmup):
+        sim.step(None)
+    barrier.wait()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sim.step(None)
+    return t0, time.perf_counter()
+
+
+def cpu_reference_parallel(scenario_key, envs_per_worker, steps, warmup, workers) -> dict:
+    """The reference's CPU step on every host core: one process per core,
+    each an independent BatchSim over its own lanes (the reference's own
+    parallel bench, rollout.py:384-409, without the GIL)."""
+    import multiprocessing as mproc
+    import numpy as np
+
+    ctx = mproc.get_context("fork")
+    mgr = ctx.Manager()
+    barrier = mgr.Barrier(workers)
+    jobs = [(scenario_key, envs_per_worker, steps, warmup, k * envs_per_worker, barrier)
+            for k in range(workers)]
+    with ctx.Pool(workers) as pool:
+        spans = pool.map(_ref_worker, jobs)
+    t0 = min(s for s, _ in spans)
+    t1 = max(e for _, e in spans)
+    envs = envs_per_worker * workers
+    return {"env_steps_per_s": envs * steps / (t1 - t0), "seconds": t1 - t0, "envs": envs,
+            "steps": steps, "workers": workers, "numpy": np.__version__}
+
+
 def run_reference_arm(args) -> int:
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    envs = args.cpu_envs
-    r = cpu_reference(args.scenario, envs, max(args.steps, 1), max(args.warmup, 1))
-    sc_units = r["n_units"]
+    workers = args.cpu_workers or (os.cpu_count() or 1)
+    r = cpu_reference_parallel(args.scenario, args.cpu_envs, max(args.steps, 1),
+                               max(args.warmup, 1), workers)
+    from paper_2602_01665_b200.scenario import builtin_scenario
+    sc_units = len(builtin_scenario(SCENARIOS[args.scenario]).units)
     v = r["env_steps_per_s"]
     line = {
         "metric": "env_steps_per_s", "value": v, "unit": "env-steps/s", "n_gpus": args.gpus,
@@ -151,10 +195,11 @@ def run_reference_arm(args) -> int:
         "data": "synthetic (scenario JSON, seeded lanes)", "impl": "reference",
         "agent_steps_per_s": v * sc_units,
         "config": {"workload": WORKLOAD[args.scenario], "scenario": SCENARIOS[args.scenario],
-                   "envs": envs, "host_threads": 1},
-        "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": 1, "kind": "port",
-                         "sample": f"{envs} envs x {r['steps']} steps (+{max(args.warmup, 1)} "
-                                   f"warm-up), oracle/tabx_oracle.py numpy {r['numpy']}"},
+                   "envs": r["envs"], "host_processes": workers},
+        "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": workers, "kind": "port",
+                         "sample": f"{workers} processes x {args.cpu_envs} envs x {r['steps']} "
+                                   f"steps (+{max(args.warmup, 1)} warm-up), "
+                                   f"oracle/tabx_oracle.py numpy {r['numpy']}"},
         "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -260,6 +305,35 @@ def run_gpu_arm(args) -> int:
     e2e_value = total * e2e_steps / (e2e_ms / 1000.0) if e2e_steps else None
     h.sim.close()
 
+    # ---------------- C5: full rollout loop (policy + step + auto-reset), CUDA graph
+    c5 = None
+    if args.rollout_envs > 0:
+        from paper_2602_01665_b200.rollout import Rollout
+        r_total = args.rollout_envs * world
+        r_first, r_per = shard.shard_range(r_total, world, rank)
+        ro = Rollout(base, r_per, horizon=args.horizon, policy=args.policy, device=local,
+                     seed=args.seed, first_lane=r_first)
+        ro.run()  # capture + first horizon
+        barrier()
+        r0 = torch.cuda.Event(enable_timing=True)
+        r1 = torch.cuda.Event(enable_timing=True)
+        r0.record(stream)
+        for _ in range(args.rollout_iters):
+            ro.run()
+        r1.record(stream)
+        barrier()
+        r_ms = max_over_ranks(r0.elapsed_time(r1))
+        c5 = {"value": r_total * args.horizon * args.rollout_iters / (r_ms / 1000.0),
+              "unit": "env-steps/s", "envs": r_total, "horizon": args.horizon,
+              "policy": args.policy, "iterations": args.rollout_iters,
+              "ms_per_horizon": r_ms / args.rollout_iters,
+              "note": "policy forward + masked sampling + batched step + auto-reset, whole "
+                      "horizon in one CUDA graph; observations written in place into the "
+                      "[T+1,B,N,D] horizon buffer"}
+        ro.close()
+        del ro
+        torch.cuda.empty_cache()
+
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -278,7 +352,7 @@ def run_gpu_arm(args) -> int:
         prof = os.path.join(ROOT, "profiles", f"traffic_{args.scenario}.json")
         if os.path.exists(prof):
             with open(prof) as fh:
-                traffic = json.load(fh).get("bytes_per_launch")
+                traffic = json.load(fh).get("bytes_per_env_step", 0) * per or None
         line = {
             "metric": "env_steps_per_s", "value": value, "unit": "env-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
@@ -306,6 +380,8 @@ def run_gpu_arm(args) -> int:
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if c5 is not None:
+            line["rollout_c5"] = c5
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -328,8 +404,14 @@ def main(argv=None) -> int:
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-envs", type=int, default=256)
     ap.add_argument("--cpu-steps", type=int, default=40)
+    ap.add_argument("--cpu-workers", type=int, default=0, help="reference arm processes (0 = all cores)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--rollout-envs", type=int, default=16384,
+                    help="C5 rollout loop envs per GPU (0 = skip)")
+    ap.add_argument("--horizon", type=int, default=128)
+    ap.add_argument("--policy", choices=("random", "mlp"), default="mlp")
+    ap.add_argument("--rollout-iters", type=int, default=2)
     args = ap.parse_args(argv)
     if args.impl == "reference":
         return run_reference_arm(args)

@@ -1,0 +1,163 @@
+"""Full on-device rollout loop (BASELINE config C5).
+
+A trainer's collection loop with nothing on the host: each step the policy
+reads the previous observation in place, samples legal actions from the
+current action mask, and the batched step writes the next observation
+straight into the horizon buffer slot (no copies).  The whole horizon —
+policy forward, masked sampling and the environment kernels — is captured
+once into a CUDA graph and replayed per iteration.
+
+Policies: ``random`` (uniform over legal actions, the reference's random
+controller semantics) or ``mlp`` (a bf16 two-layer MLP over the per-agent
+observation, masked Gumbel-max sampling).  The ally team is driven by the
+policy (external controller); the enemy keeps its scenario controller.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as nat
+from .rng import lane_seeds
+from .scenario import Scenario
+from .sim import BatchSim
+
+
+class MLPPolicy(torch.nn.Module):
+    def __init__(self, obs_dim: int, hidden: int = 128, n_actions: int = 7):
+        super().__init__()
+        self.l1 = torch.nn.Linear(obs_dim, hidden)
+        self.l2 = torch.nn.Linear(hidden, n_actions)
+
+    def forward(self, obs: torch.Tensor) -> torch.Tensor:
+        h = torch.relu(self.l1(obs))
+        return self.l2(h)
+
+
+def masked_sample(logits: torch.Tensor, mask: torch.Tensor):
+    """Gumbel-max sample over legal actions; returns (actions int64, logp f32)."""
+    u = torch.rand_like(logits, dtype=torch.float32).clamp_(1e-12, 1.0)
+    g = -torch.log(-torch.log(u))
+    neg = torch.finfo(torch.float32).min
+    masked = torch.where(mask, logits.float(), neg)
+    act = torch.argmax(masked + g, dim=-1)
+    logp = torch.log_softmax(masked, dim=-1).gather(-1, act[..., None])[..., 0]
+    return act, logp
+
+
+@dataclass
+class RolloutBuffers:
+    observations: torch.Tensor | None  # [T+1, B, N, D] float32 (slot 0 = start)
+    actions: torch.Tensor  # [T, B, N] int64
+    logp: torch.Tensor  # [T, B, N] float32
+    rewards: torch.Tensor  # [T, B, N] float32
+    terminated: torch.Tensor  # [T, B] bool
+    truncated: torch.Tensor  # [T, B] bool
+
+
+class Rollout:
+    def __init__(self, scenario: Scenario, envs: int, horizon: int = 128, policy: str = "random",
+                 device=0, seed: int = 0, first_lane: int = 0, store_obs: bool = True,
+                 hidden: int = 128, use_graph: bool = True):
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        sc = scenario.with_controllers(ally="external")
+        self.sim = BatchSim([sc] * envs, lane_seeds(seed, envs, first_lane), auto_reset=True,
+                            device=self.device, strict=False, interactions=False,
+                            final_observations=False)
+        self.B, self.N, self.D = envs, self.sim.n_units, self.sim.obs_dim
+        self.T = horizon
+        self.kind = policy
+        dev = self.device
+        T, B, N, D = self.T, self.B, self.N, self.D
+        self.buf = RolloutBuffers(
+            observations=torch.empty(T + 1, B, N, D, device=dev) if store_obs else None,
+            actions=torch.empty(T, B, N, dtype=torch.int64, device=dev),
+            logp=torch.empty(T, B, N, device=dev),
+            rewards=torch.empty(T, B, N, device=dev),
+            terminated=torch.empty(T, B, dtype=torch.bool, device=dev),
+            truncated=torch.empty(T, B, dtype=torch.bool, device=dev))
+        self.policy = None
+        if policy == "mlp":
+            self.policy = MLPPolicy(D, hidden).to(dev).to(torch.bfloat16)
+        elif policy != "random":
+            raise ValueError(f"unknown policy {policy!r}")
+        self._outs = []
+        for t in range(T):
+            o = nat.TabxOutputs()
+            for k in nat.OUTPUT_FIELDS:
+                setattr(o, k, None)
+            obs = self.buf.observations[t + 1] if store_obs else self.sim._buf["observations"]
+            o.observations = obs.data_ptr()
+            o.global_state = self.sim._buf["global_state"].data_ptr()
+            o.rewards = self.buf.rewards[t].data_ptr()
+            o.action_mask = self.sim._buf["action_mask"].data_ptr()
+            o.terminated = self.buf.terminated[t].data_ptr()
+            o.truncated = self.buf.truncated[t].data_ptr()
+            o.done = self.sim._buf["done"].data_ptr()
+            o.reset_mask = self.sim._buf["reset_mask"].data_ptr()
+            self._outs.append(o)
+        if store_obs:
+            self.buf.observations[0].copy_(self.sim._buf["observations"])
+        self.graph = None
+        self.use_graph = use_graph
+
+    def _current_obs(self, t):
+        if self.buf.observations is not None:
+            return self.buf.observations[t]
+        return self.sim._buf["observations"]
+
+    def _step(self, t):
+        mask = self.sim._buf["action_mask"]
+        obs = self._current_obs(t)
+        if self.policy is None:
+            logits = torch.zeros(self.B, self.N, 7, device=self.device)
+        else:
+            logits = self.policy(obs.to(torch.bfloat16))
+        act, logp = masked_sample(logits, mask)
+        self.buf.actions[t].copy_(act)
+        self.buf.logp[t].copy_(logp)
+        L = nat.lib()
+        nat.check(L.tabx_step(self.sim.handle, ct.c_void_p(self.buf.actions[t].data_ptr()),
+                              ct.byref(self._outs[t])), "tabx_step")
+
+    def _horizon(self):
+        for t in range(self.T):
+            self._step(t)
+
+    def _set_stream(self, stream):
+        nat.check(nat.lib().tabx_set_stream(self.sim.handle, ct.c_void_p(stream.cuda_stream)),
+                  "tabx_set_stream")
+
+    def capture(self) -> None:
+        """Record the whole horizon into one CUDA graph (after a warm-up run)."""
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self._set_stream(s)
+            self._horizon()  # warm-up: cuBLAS handles, allocator pools
+            if self.buf.observations is not None:
+                self.buf.observations[0].copy_(self.buf.observations[self.T])
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._set_stream(torch.cuda.current_stream(self.device))
+            self._horizon()
+        self._set_stream(torch.cuda.current_stream(self.device))
+
+    def run(self) -> RolloutBuffers:
+        """Collect one horizon (graph replay when captured)."""
+        if self.use_graph:
+            if self.graph is None:
+                self.capture()
+            self.graph.replay()
+        else:
+            self._horizon()
+        if self.buf.observations is not None:
+            # next horizon starts from the last observation
+            self.buf.observations[0].copy_(self.buf.observations[self.T])
+        return self.buf
+
+    def close(self):
+        self.sim.close()
