@@ -111,7 +111,7 @@ static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
   int R = budget / (4 * h->D);
   if (R < 1) R = 1;
   if (R > h->N) R = h->N;
-  int need = (R * h->D > h->G ? R * h->D : h->G) + 3;
+  int need = (R * h->D > h->G ? R * h->D : h->G) + 8;
   P.stage_rows = R;
   P.stage_floats = (need + 3) & ~3;
   return P;

@@ -52,13 +52,17 @@ struct EnvSmem {
   static constexpr int NT = 32 * W;
   double px[NT], py[NT], ch[NT], sh[NT], rad[NT], mh[NT], rv[NT], dmg[NT];
   double vx[NT], vy[NT], sx[NT], sy[NT];
-  float own[NT][TABX_OWN_DIM];
+  float own[NT][16] __attribute__((aligned(16)));  // 15 own features + pad
   uint32_t vis[NT * W], atk[NT * W], touch[NT * W];
   uint32_t uf[NT];
   uint32_t zin[NT];
   int32_t tgt[NT];
   uint32_t ball[W];
+  // env-wide unit sets as N-bit masks (word k = units 32k..32k+31)
+  uint32_t m_active[W], m_alive[W], m_enemy[W], m_rev[W], m_inbush[W];
+  uint32_t m_zone[TABX_MAX_ZONES][W];
   double red[2];
+  double part[16];
 };
 
 template <int W>
@@ -103,6 +107,34 @@ __device__ __forceinline__ int env_count(bool p, EnvSmem<W>& S, int i) {
 #pragma unroll
   for (int k = 0; k < W; ++k) c += __popc(m[k]);
   return c;
+}
+
+// Env-wide unit masks from the per-unit state just published (all threads).
+template <int W>
+__device__ __forceinline__ void build_masks(EnvSmem<W>& S, int i, bool valid, bool active,
+                                            bool alive, bool enemy, double rv, uint32_t zin,
+                                            int Z, uint32_t bush_m) {
+  uint32_t m[W];
+  env_ballot<W>(valid && active, S, i, m);
+  if ((i & 31) == 0) S.m_active[i >> 5] = m[i >> 5];
+  env_ballot<W>(valid && alive, S, i, m);
+  if ((i & 31) == 0) S.m_alive[i >> 5] = m[i >> 5];
+  env_ballot<W>(valid && enemy, S, i, m);
+  if ((i & 31) == 0) S.m_enemy[i >> 5] = m[i >> 5];
+  env_ballot<W>(valid && rv > 0.0, S, i, m);
+  if ((i & 31) == 0) S.m_rev[i >> 5] = m[i >> 5];
+  uint32_t inb[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) inb[k] = 0u;
+  for (int z = 0; z < Z; ++z) {
+    env_ballot<W>(valid && ((zin >> z) & 1u), S, i, m);
+    if ((i & 31) == 0) S.m_zone[z][i >> 5] = m[i >> 5];
+    if ((bush_m >> z) & 1u) {
+#pragma unroll
+      for (int k = 0; k < W; ++k) inb[k] |= m[k];
+    }
+  }
+  if ((i & 31) == 0) S.m_inbush[i >> 5] = inb[i >> 5];
 }
 
 __device__ __forceinline__ bool bit_of(const uint32_t* row, int j) {
@@ -259,12 +291,14 @@ static __device__ __noinline__ bool exact_box(double dx, double dy, double ch, d
 // target (perception.py:52-96, combat.py:16-83).  Writes the two N-bit rows
 // to S.vis / S.atk and returns the target or -1.
 //
-// Each pair is first classified in float32 (range against sight_range^2,
-// view wedge via rsqrt, strike box) with margins two orders of magnitude
-// above the float32 error bound; only pairs inside a margin (and the few
-// attackable pairs, whose exact distance orders the target choice) are
-// evaluated with the reference's float64 expressions.  The verdicts are
-// therefore exactly the float64 ones.
+// Pass 1 (branch-free over all j): classify each pair in float32 -- sight
+// range against sight_range^2, view wedge via rsqrt -- with margins two orders
+// of magnitude above the float32 error bound, into "surely seen" and "unsure"
+// bit masks.  Pass 2 evaluates the rare unsure pairs with the reference's
+// float64 expressions.  Bush concealment is then pure mask algebra over the
+// env-wide masks, and the strike box + exact distance (which orders the
+// target) run only over the few attackable candidates.  Verdicts are exactly
+// the float64 ones.
 template <int W>
 __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, double cos_half,
                                               double srange, double dmg, double reach, double rad,
@@ -281,70 +315,94 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
     const float sr2_lo = sr2 * 0.99999f, sr2_hi = sr2 * 1.00001f;
     const float cf = (float)cos_half;
     const float cf_lo = cf - 2e-5f, cf_hi = cf + 2e-5f;
-    const float reachf = (float)reach, radf = (float)rad;
-    const bool enemy_i = (uf_i & UF_ENEMY) != 0;
-    const bool can_hit = (uf_i & UF_ALIVE) && dmg != 0.0;
-    const uint32_t bush_i = S.zin[i] & bush_m;
-    double best = 0.0;
-    // the diagonal: distance 0, cos_dev 1 -> visible, never attackable
-    vis[i >> 5] |= 1u << (i & 31);
+    uint32_t seen[W], unsure[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) seen[k] = unsure[k] = 0u;
+#pragma unroll 4
     for (int j = 0; j < N; ++j) {
-      const uint32_t uj = S.uf[j];
-      if (!(uj & UF_ACTIVE) || j == i) continue;
-      const double dx = S.px[j] - px;
-      const double dy = S.py[j] - py;
-      const float dxf = (float)dx, dyf = (float)dy;
+      const float dxf = (float)(S.px[j] - px), dyf = (float)(S.py[j] - py);
       const float d2f = dxf * dxf + dyf * dyf;
-      if (d2f >= sr2_hi && d2f > 0.0f) continue;  // certainly beyond sight range
-      const float lxf = dxf * chf + dyf * shf;
-      double dist = -1.0;
-      bool seen;
-      bool exact = true;
-      if (d2f > 1e-30f && d2f <= sr2_lo) {
-        const float cdevf = lxf * rsqrtf(d2f);
-        if (cdevf >= cf_hi) {
-          seen = true;
-          exact = false;
-        } else if (cdevf <= cf_lo) {
-          seen = false;
-          exact = false;
+      const float cdevf = (dxf * chf + dyf * shf) * rsqrtf(d2f);
+      const bool inr = (d2f <= sr2_lo) & (d2f > 1e-30f);
+      const bool outr = (d2f >= sr2_hi) & (d2f > 0.0f);
+      const bool wt = cdevf >= cf_hi, wf = cdevf <= cf_lo;
+      seen[j >> 5] |= (uint32_t)(inr & wt) << (j & 31);
+      unsure[j >> 5] |= (uint32_t)(!outr & !(inr & (wt | wf))) << (j & 31);
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const uint32_t keep = S.m_active[k] & ~(k == (i >> 5) ? 1u << (i & 31) : 0u);
+      seen[k] &= keep;
+      unsure[k] &= keep;
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      uint32_t m = unsure[k];
+      while (m) {
+        const int j = (k << 5) + __ffs(m) - 1;
+        m &= m - 1;
+        const Seen e = exact_seen(S.px[j] - px, S.py[j] - py, ch, sh, srange, cos_half);
+        if (e.seen) seen[k] |= 1u << (j & 31);
+      }
+    }
+    // concealment: j in a bush, on the other team, not sharing a bush with i,
+    // reveal timer run out (perception.py:86-96)
+    const bool enemy_i = (uf_i & UF_ENEMY) != 0;
+    const uint32_t bush_i = S.zin[i] & bush_m;
+    uint32_t shared[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) shared[k] = 0u;
+    for (uint32_t zb = bush_i; zb; zb &= zb - 1) {
+      const int z = __ffs(zb) - 1;
+#pragma unroll
+      for (int k = 0; k < W; ++k) shared[k] |= S.m_zone[z][k];
+    }
+    const bool can_hit = (uf_i & UF_ALIVE) && dmg != 0.0;
+    uint32_t cand[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      const uint32_t foe = enemy_i ? ~S.m_enemy[k] : S.m_enemy[k];
+      const uint32_t hidden = S.m_inbush[k] & foe & ~shared[k] & ~S.m_rev[k];
+      vis[k] = seen[k] & ~hidden;
+      const uint32_t role = dmg > 0.0 ? foe : ~foe;
+      cand[k] = can_hit ? (vis[k] & role & S.m_alive[k]) : 0u;
+    }
+    vis[i >> 5] |= 1u << (i & 31);  // distance 0, cos_dev 1: sees itself
+    const float reachf = (float)reach, radf = (float)rad;
+    double best = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      uint32_t m = cand[k];
+      while (m) {
+        const int j = (k << 5) + __ffs(m) - 1;
+        m &= m - 1;
+        const double dx = S.px[j] - px;
+        const double dy = S.py[j] - py;
+        const double rj = S.rad[j];
+        const float dxf = (float)dx, dyf = (float)dy, rjf = (float)rj;
+        const float lxf = dxf * chf + dyf * shf;
+        const float lyf = (-dxf) * shf + dyf * chf;
+        const float gxf = lxf - fminf(fmaxf(lxf, 0.0f), reachf);
+        const float gyf = lyf - fminf(fmaxf(lyf, -radf), radf);
+        const float gapf = gxf * gxf + gyf * gyf;
+        const float rj2f = rjf * rjf;
+        const float L = fabsf(lxf) + fabsf(lyf) + reachf + radf + rjf;
+        const float mb = 3e-5f * L * L;
+        bool box;
+        if (gapf < rj2f - mb) {
+          box = true;
+        } else if (gapf > rj2f + mb) {
+          box = false;
+        } else {
+          box = exact_box(dx, dy, ch, sh, reach, rad, rj);
         }
-      }
-      if (exact) {
-        const Seen e = exact_seen(dx, dy, ch, sh, srange, cos_half);
-        dist = e.dist;
-        seen = e.seen;
-      }
-      if (!seen) continue;
-      const bool foe = ((uj & UF_ENEMY) != 0) != enemy_i;
-      const uint32_t bush_j = S.zin[j] & bush_m;
-      if (bush_j != 0u && foe && (bush_i & bush_j) == 0u && S.rv[j] <= 0.0) continue;
-      vis[j >> 5] |= 1u << (j & 31);
-      const bool role = dmg > 0.0 ? foe : !foe;
-      if (!(can_hit && role && (uj & UF_ALIVE))) continue;
-      const double rj = S.rad[j];
-      const float rjf = (float)rj;
-      const float lyf = (-dxf) * shf + dyf * chf;
-      const float gxf = lxf - fminf(fmaxf(lxf, 0.0f), reachf);
-      const float gyf = lyf - fminf(fmaxf(lyf, -radf), radf);
-      const float gapf = gxf * gxf + gyf * gyf;
-      const float rj2f = rjf * rjf;
-      const float L = fabsf(lxf) + fabsf(lyf) + reachf + radf + rjf;
-      const float mb = 3e-5f * L * L;
-      bool box;
-      if (gapf < rj2f - mb) {
-        box = true;
-      } else if (gapf > rj2f + mb) {
-        box = false;
-      } else {
-        box = exact_box(dx, dy, ch, sh, reach, rad, rj);
-      }
-      if (!box) continue;
-      atk[j >> 5] |= 1u << (j & 31);
-      if (dist < 0.0) dist = slow_sqrt(dx * dx + dy * dy);
-      if (tgt < 0 || dist < best) {
-        best = dist;
-        tgt = j;
+        if (!box) continue;
+        atk[k] |= 1u << (j & 31);
+        const double dist = sqrt(dx * dx + dy * dy);
+        if (tgt < 0 || dist < best) {
+          best = dist;
+          tgt = j;
+        }
       }
     }
   }
@@ -427,7 +485,11 @@ __device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs,
 
 // Observation rows of one environment (perception.py:159-192) and its
 // global-state row (perception.py:194-200), from S.own / S.vis / S.atk /
-// positions.  R rows per chunk; SF floats per stage buffer.
+// positions.  R rows per chunk; SF floats per stage buffer.  Each chunk is
+// zero-filled with 16-byte stores, then only the visible (observer, other)
+// pairs are written -- enumerated straight from the N-bit visibility rows
+// (popc prefix over the chunk's rows + __fns), so every lane works on a
+// visible pair and hidden pairs cost nothing beyond the zero fill.
 template <int W>
 __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* __restrict__ glob,
                                                int64_t b, int N, int Z, int D, int G, int R,
@@ -444,62 +506,78 @@ __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* _
       const int nr = min(R, N - r0);
       const int64_t gs = (b * N + r0) * (int64_t)D;
       float* st = stage + buf * SF;
-      float* row0 = st + (int)(gs & 3);
+      const int pad = (int)(gs & 3);
+      float* row0 = st + pad;
       if (tid == 0) bulk_wait_read<1>();
+      env_sync<W>();
+      {
+        const int n4 = (pad + nr * D + 3) >> 2;
+        float4* z4 = reinterpret_cast<float4*>(st);
+        for (int q = tid; q < n4; q += NT) z4[q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      }
       env_sync<W>();
       for (int e = tid; e < nr * TABX_OWN_DIM; e += NT) {
         const int rr = e / TABX_OWN_DIM, f = e - rr * TABX_OWN_DIM;
         row0[rr * D + f] = S.own[r0 + rr][f];
       }
-      if (M > 0) {
-        const int qd = NT / M, qm = NT % M;
-        int rr = tid / M, k = tid - (tid / M) * M;
-        for (int p = tid; p < nr * M; p += NT) {
+      // visible pairs of the chunk's rows (vis excludes inactive rows/columns)
+      int total = 0;
+      for (int rr = 0; rr < nr; ++rr) {
+        const int r = r0 + rr;
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+          total += __popc(S.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u));
+      }
+      for (int s = tid; s < total; s += NT) {
+        int rr = 0, n = s, j = -1;
+        for (; rr < nr; ++rr) {
           const int r = r0 + rr;
-          const int j = k + (k >= r ? 1 : 0);
-          float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * k;
-          const uint32_t uj = S.uf[j];
-          const bool show = (S.uf[r] & UF_ACTIVE) && bit_of(&S.vis[r * W], j) && (uj & UF_ACTIVE);
-          if (show) {
-            const float* oj = S.own[j];
-            blk[0] = oj[0];
-            blk[1] = oj[1];
-            blk[2] = f32_quot(S.px[j] - S.px[r], fw, rw);
-            blk[3] = f32_quot(S.py[j] - S.py[r], fh, rh);
-#pragma unroll
-            for (int f = 4; f < TABX_OWN_DIM; ++f) blk[f] = oj[f];
-            blk[15] = (uj & UF_ENEMY) ? 1.0f : 0.0f;
-            blk[16] = bit_of(&S.atk[r * W], j) ? 1.0f : 0.0f;
-          } else {
-#pragma unroll
-            for (int f = 0; f < TABX_OTHER_DIM; ++f) blk[f] = 0.0f;
+          for (int k = 0; k < W && j < 0; ++k) {
+            const uint32_t w = S.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u);
+            const int c = __popc(w);
+            if (n < c) {
+              j = (k << 5) + (int)__fns(w, 0, n + 1);
+            } else {
+              n -= c;
+            }
           }
-          rr += qd;
-          k += qm;
-          if (k >= M) {
-            k -= M;
-            ++rr;
-          }
+          if (j >= 0) break;
         }
+        const int r = r0 + rr;
+        const int kk = j - (j > r ? 1 : 0);
+        float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
+        const float4* oj = reinterpret_cast<const float4*>(S.own[j]);
+        const float4 o0 = oj[0], o1 = oj[1], o2 = oj[2], o3 = oj[3];
+        blk[0] = o0.x;
+        blk[1] = o0.y;
+        blk[2] = f32_quot(S.px[j] - S.px[r], fw, rw);
+        blk[3] = f32_quot(S.py[j] - S.py[r], fh, rh);
+        blk[4] = o1.x;
+        blk[5] = o1.y;
+        blk[6] = o1.z;
+        blk[7] = o1.w;
+        blk[8] = o2.x;
+        blk[9] = o2.y;
+        blk[10] = o2.z;
+        blk[11] = o2.w;
+        blk[12] = o3.x;
+        blk[13] = o3.y;
+        blk[14] = o3.z;
+        blk[15] = (S.uf[j] & UF_ENEMY) ? 1.0f : 0.0f;
+        blk[16] = bit_of(&S.atk[r * W], j) ? 1.0f : 0.0f;
       }
       for (int q = tid; q < nr * Z; q += NT) {
         const int rr = q / Z, z = q - rr * Z;
         const int r = r0 + rr;
-        float* blk = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
         const int ty = C->zone_type[z];
-        if (ty != TABX_ZONE_NONE && (S.uf[r] & UF_ACTIVE)) {
-          blk[0] = ty == 1 ? 1.0f : 0.0f;
-          blk[1] = ty == 2 ? 1.0f : 0.0f;
-          blk[2] = ty == 3 ? 1.0f : 0.0f;
-          blk[3] = f32_quot(C->zone_cx[z] - S.px[r], fw, rw);
-          blk[4] = f32_quot(C->zone_cy[z] - S.py[r], fh, rh);
-          blk[5] = __double2float_rn(C->zone_ax[z]);
-          blk[6] = __double2float_rn(C->zone_ay[z]);
-          blk[7] = __double2float_rn(C->zone_effect[z]);
-        } else {
-#pragma unroll
-          for (int f = 0; f < TABX_ZONE_DIM; ++f) blk[f] = 0.0f;
-        }
+        if (ty == TABX_ZONE_NONE || !(S.uf[r] & UF_ACTIVE)) continue;  // stays zero
+        float* blk = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
+        blk[ty - 1] = 1.0f;
+        blk[3] = f32_quot(C->zone_cx[z] - S.px[r], fw, rw);
+        blk[4] = f32_quot(C->zone_cy[z] - S.py[r], fh, rh);
+        blk[5] = __double2float_rn(C->zone_ax[z]);
+        blk[6] = __double2float_rn(C->zone_ay[z]);
+        blk[7] = __double2float_rn(C->zone_effect[z]);
       }
       fence_proxy_async();
       env_sync<W>();
@@ -513,8 +591,10 @@ __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* _
     float* row = st + (int)(gs & 3);
     if (tid == 0) bulk_wait_read<1>();
     env_sync<W>();
-    const float* own = &S.own[0][0];
-    for (int e = tid; e < N * TABX_OWN_DIM; e += NT) row[e] = own[e];
+    for (int e = tid; e < N * TABX_OWN_DIM; e += NT) {
+      const int u = e / TABX_OWN_DIM;
+      row[e] = S.own[u][e - u * TABX_OWN_DIM];
+    }
     for (int q = tid; q < Z * TABX_ZONE_DIM; q += NT) {
       const int z = q >> 3, f = q & 7;
       const int ty = C->zone_type[z];
@@ -546,6 +626,7 @@ __device__ __forceinline__ void own_features(float* o, const UnitStatic& U, doub
                                              double rucd, double hp, double px, double py,
                                              double ch, double sh, double cd, bool alive,
                                              double fw, double fh, double rw, double rh) {
+  o[15] = 0.0f;
   if (!U.active) {
 #pragma unroll
     for (int f = 0; f < TABX_OWN_DIM; ++f) o[f] = 0.0f;
@@ -577,9 +658,27 @@ __device__ __forceinline__ void team_ratios(EnvSmem<W>& S, int i, int N, bool ac
   S.vx[i] = (active && !enemy) ? hp / mh : 0.0;
   S.vy[i] = (active && enemy) ? hp / mh : 0.0;
   env_sync<W>();
-  if (i == 0) {
-    double ca = (double)(n_ally > 1 ? n_ally : 1);
-    double ce = (double)(n_enemy > 1 ? n_enemy : 1);
+  const double ca = (double)(n_ally > 1 ? n_ally : 1);
+  const double ce = (double)(n_enemy > 1 ? n_enemy : 1);
+  if (W == 1 && N >= 8) {
+    // numpy's 8-accumulator block (n <= 128): lanes 0-7 / 8-15 run the ally /
+    // enemy accumulators, lanes 0 and 8 combine them in numpy's tree order
+    const int lim = N - (N % 8);
+    if (i < 16) {
+      const double* v = i < 8 ? S.vx : S.vy;
+      double r = v[i & 7];
+      for (int q = 8 + (i & 7); q < lim; q += 8) r += v[q];
+      S.part[i] = r;
+    }
+    env_sync<W>();
+    if (i == 0 || i == 8) {
+      const double* v = i == 0 ? S.vx : S.vy;
+      const double* pp = S.part + i;
+      double r = ((pp[0] + pp[1]) + (pp[2] + pp[3])) + ((pp[4] + pp[5]) + (pp[6] + pp[7]));
+      for (int q = lim; q < N; ++q) r += v[q];
+      S.red[i >> 3] = r / (i == 0 ? ca : ce);
+    }
+  } else if (i == 0) {
     S.red[0] = pairwise_sum(S.vx, N) / ca;
     S.red[1] = pairwise_sum(S.vy, N) / ce;
   }
@@ -602,10 +701,12 @@ __device__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restric
   // squared distances; closer() orders them exactly as their float64 roots
   double bf = 0.0, bi = 0.0, bn = 0.0, bm = 0.0, bmd = 0.0;
   int tf = -1, ti = -1, tn = -1, tm = -1;
-  for (int j = 0; j < N; ++j) {
+  for (int k = 0; k < W; ++k) {
+   uint32_t cm = vis[k] & S.m_active[k] & S.m_alive[k] & ~(k == (i >> 5) ? 1u << (i & 31) : 0u);
+   while (cm) {
+    const int j = (k << 5) + __ffs(cm) - 1;
+    cm &= cm - 1;
     const uint32_t uj = S.uf[j];
-    if (j == i || !bit_of(vis, j) || (uj & (UF_ACTIVE | UF_ALIVE)) != (UF_ACTIVE | UF_ALIVE))
-      continue;
     const double dx = S.px[j] - px, dy = S.py[j] - py;
     const double d = dx * dx + dy * dy;
     const bool foe = ((uj & UF_ENEMY) != 0) != U.enemy;
@@ -617,6 +718,7 @@ __device__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restric
       const double m = S.mh[j];
       if (tm < 0 || m < bm || (m == bm && closer(d, bmd))) { bm = m; bmd = d; tm = j; }
     }
+   }
   }
   int tgt;
   bool has;
@@ -771,6 +873,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   if (P.mode != MODE_STEP) {
     // init_output / refresh_caches (environment.py:147-151, :351-374)
     publish();
+    build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
     env_sync<W>();
     if (P.mode == MODE_REFRESH) {
       if (refresh) {
@@ -836,6 +939,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 
   // ======================= step (environment.py:207-348) ==================
   publish();
+    build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
   env_sync<W>();
 
   // 1. pre-step action mask (arrays.py:373-387)
@@ -907,28 +1011,34 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   for (int k = 0; k < W; ++k) trow[k] = 0u;
   bool any_touch = false;
   if (valid && U.active && running) {
+    // float32 filter on squared distance vs rs^2 (margin 1e-5 relative);
+    // near-contact pairs get the reference's float64 depth test
+    uint32_t unsure[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) unsure[k] = 0u;
     for (int j = i + 1; j < N; ++j) {
-      if (!(S.uf[j] & UF_ACTIVE)) continue;
-      const double dx = S.px[j] - px, dy = S.py[j] - py;
-      const double rs = U.rad + S.rad[j];
-      // float32 filter on squared distance vs rs^2 (margin 1e-5 relative);
-      // near-contact pairs get the reference's float64 depth test
-      const float dxf = (float)dx, dyf = (float)dy;
+      const float dxf = (float)(S.px[j] - px), dyf = (float)(S.py[j] - py);
       const float d2f = dxf * dxf + dyf * dyf;
-      const float rs2f = (float)(rs * rs);
-      if (d2f > rs2f * 1.00001f) continue;
-      bool hit;
-      if (d2f < rs2f * 0.99999f && d2f > 1e-30f) {
-        hit = true;
-      } else {
+      const float rs2f = (float)((U.rad + S.rad[j]) * (U.rad + S.rad[j]));
+      const bool sure = (d2f < rs2f * 0.99999f) & (d2f > 1e-30f);
+      const bool maybe = !sure & !(d2f > rs2f * 1.00001f);
+      trow[j >> 5] |= (uint32_t)sure << (j & 31);
+      unsure[j >> 5] |= (uint32_t)maybe << (j & 31);
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      trow[k] &= S.m_active[k];
+      uint32_t m = unsure[k] & S.m_active[k];
+      while (m) {
+        const int j = (k << 5) + __ffs(m) - 1;
+        m &= m - 1;
+        const double dx = S.px[j] - px, dy = S.py[j] - py;
+        const double rs = U.rad + S.rad[j];
         const double dist = slow_sqrt(dx * dx + dy * dy);
         const double depth = dist == 0.0 ? rs : rs - dist;
-        hit = depth > 0.0;
+        if (depth > 0.0) trow[k] |= 1u << (j & 31);
       }
-      if (hit) {
-        trow[j >> 5] |= 1u << (j & 31);
-        any_touch = true;
-      }
+      any_touch |= trow[k] != 0u;
     }
   }
   double vfx = vux, vfy = vuy;
@@ -1006,6 +1116,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   zin = valid ? zone_bits(C, DC, Z, px, py) : 0u;
   env_sync<W>();
   publish();
+    build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
   env_sync<W>();
   tgt = cache_row_inl<W>(S, i, N, U, bush_m);
 #pragma unroll
@@ -1156,6 +1267,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     sh = libm_sin(hd);
     zin = valid ? zone_bits(C, DC, Z, px, py) : 0u;
     publish();
+    build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
     env_sync<W>();
     cache_row_of<W>(S, i, N, U, bush_m);
 #pragma unroll
