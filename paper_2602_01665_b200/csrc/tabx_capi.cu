@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -47,6 +48,7 @@ struct tabx_handle {
   Sync* sync = nullptr;
   double* stats_dev = nullptr;
   const int64_t* last_actions = nullptr;
+  int stage_bytes = 6144;  // observation staging bytes per buffer per env
 };
 
 static thread_local std::string g_err;
@@ -107,7 +109,7 @@ static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
   P.auto_reset = h->auto_reset;
   P.mode = mode;
   // observation staging: R rows per chunk, two buffers per environment
-  const int budget = h->W == 1 ? 6144 : 16384;
+  const int budget = h->stage_bytes;
   int R = budget / (4 * h->D);
   if (R < 1) R = 1;
   if (R > h->N) R = h->N;
@@ -186,6 +188,8 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   h->D = tabx_obs_dim(N, Z);
   h->G = tabx_global_dim(N, Z);
   h->auto_reset = auto_reset ? 1 : 0;
+  h->stage_bytes = h->W == 1 ? 6144 : 16384;
+  if (const char* sb = getenv("TABX_STAGE_BYTES")) h->stage_bytes = atoi(sb);
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
 
   const int64_t B = batch, U = batch * N, W = h->W;

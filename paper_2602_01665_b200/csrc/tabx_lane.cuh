@@ -520,64 +520,48 @@ __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* _
         const int rr = e / TABX_OWN_DIM, f = e - rr * TABX_OWN_DIM;
         row0[rr * D + f] = S.own[r0 + rr][f];
       }
-      // visible pairs of the chunk's rows (vis excludes inactive rows/columns)
-      int total = 0;
+      // visible pairs, one row at a time: thread j owns column j, so only the
+      // (few) visible pairs of the row execute the block write
       for (int rr = 0; rr < nr; ++rr) {
         const int r = r0 + rr;
-#pragma unroll
-        for (int k = 0; k < W; ++k)
-          total += __popc(S.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u));
-      }
-      for (int s = tid; s < total; s += NT) {
-        int rr = 0, n = s, j = -1;
-        for (; rr < nr; ++rr) {
-          const int r = r0 + rr;
-          for (int k = 0; k < W && j < 0; ++k) {
-            const uint32_t w = S.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u);
-            const int c = __popc(w);
-            if (n < c) {
-              j = (k << 5) + (int)__fns(w, 0, n + 1);
-            } else {
-              n -= c;
-            }
-          }
-          if (j >= 0) break;
+        const int j = tid;
+        if (j < N && j != r && bit_of(&S.vis[r * W], j)) {
+          const int kk = j - (j > r ? 1 : 0);
+          float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
+          const float4* oj = reinterpret_cast<const float4*>(S.own[j]);
+          const float4 o0 = oj[0], o1 = oj[1], o2 = oj[2], o3 = oj[3];
+          blk[0] = o0.x;
+          blk[1] = o0.y;
+          blk[2] = f32_quot(S.px[j] - S.px[r], fw, rw);
+          blk[3] = f32_quot(S.py[j] - S.py[r], fh, rh);
+          blk[4] = o1.x;
+          blk[5] = o1.y;
+          blk[6] = o1.z;
+          blk[7] = o1.w;
+          blk[8] = o2.x;
+          blk[9] = o2.y;
+          blk[10] = o2.z;
+          blk[11] = o2.w;
+          blk[12] = o3.x;
+          blk[13] = o3.y;
+          blk[14] = o3.z;
+          blk[15] = (S.uf[j] & UF_ENEMY) ? 1.0f : 0.0f;
+          blk[16] = bit_of(&S.atk[r * W], j) ? 1.0f : 0.0f;
         }
-        const int r = r0 + rr;
-        const int kk = j - (j > r ? 1 : 0);
-        float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
-        const float4* oj = reinterpret_cast<const float4*>(S.own[j]);
-        const float4 o0 = oj[0], o1 = oj[1], o2 = oj[2], o3 = oj[3];
-        blk[0] = o0.x;
-        blk[1] = o0.y;
-        blk[2] = f32_quot(S.px[j] - S.px[r], fw, rw);
-        blk[3] = f32_quot(S.py[j] - S.py[r], fh, rh);
-        blk[4] = o1.x;
-        blk[5] = o1.y;
-        blk[6] = o1.z;
-        blk[7] = o1.w;
-        blk[8] = o2.x;
-        blk[9] = o2.y;
-        blk[10] = o2.z;
-        blk[11] = o2.w;
-        blk[12] = o3.x;
-        blk[13] = o3.y;
-        blk[14] = o3.z;
-        blk[15] = (S.uf[j] & UF_ENEMY) ? 1.0f : 0.0f;
-        blk[16] = bit_of(&S.atk[r * W], j) ? 1.0f : 0.0f;
-      }
-      for (int q = tid; q < nr * Z; q += NT) {
-        const int rr = q / Z, z = q - rr * Z;
-        const int r = r0 + rr;
-        const int ty = C->zone_type[z];
-        if (ty == TABX_ZONE_NONE || !(S.uf[r] & UF_ACTIVE)) continue;  // stays zero
-        float* blk = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
-        blk[ty - 1] = 1.0f;
-        blk[3] = f32_quot(C->zone_cx[z] - S.px[r], fw, rw);
-        blk[4] = f32_quot(C->zone_cy[z] - S.py[r], fh, rh);
-        blk[5] = __double2float_rn(C->zone_ax[z]);
-        blk[6] = __double2float_rn(C->zone_ay[z]);
-        blk[7] = __double2float_rn(C->zone_effect[z]);
+        // zone blocks of row r: thread z (stay zero for unused slots / inactive rows)
+        if (tid < Z && (S.uf[r] & UF_ACTIVE)) {
+          const int z = tid;
+          const int ty = C->zone_type[z];
+          if (ty != TABX_ZONE_NONE) {
+            float* zb = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
+            zb[ty - 1] = 1.0f;
+            zb[3] = f32_quot(C->zone_cx[z] - S.px[r], fw, rw);
+            zb[4] = f32_quot(C->zone_cy[z] - S.py[r], fh, rh);
+            zb[5] = __double2float_rn(C->zone_ax[z]);
+            zb[6] = __double2float_rn(C->zone_ay[z]);
+            zb[7] = __double2float_rn(C->zone_effect[z]);
+          }
+        }
       }
       fence_proxy_async();
       env_sync<W>();
