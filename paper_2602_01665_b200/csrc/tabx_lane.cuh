@@ -109,6 +109,21 @@ __device__ __forceinline__ int env_count(bool p, EnvSmem<W>& S, int i) {
   return c;
 }
 
+// Position of the n-th (0-based) set bit of w, by popc halving.
+__device__ __forceinline__ int nth_set_bit(uint32_t w, int n) {
+  int pos = 0;
+  int c = __popc(w & 0xFFFFu);
+  if (n >= c) { n -= c; w >>= 16; pos += 16; }
+  c = __popc(w & 0xFFu);
+  if (n >= c) { n -= c; w >>= 8; pos += 8; }
+  c = __popc(w & 0xFu);
+  if (n >= c) { n -= c; w >>= 4; pos += 4; }
+  c = __popc(w & 0x3u);
+  if (n >= c) { n -= c; w >>= 2; pos += 2; }
+  if (n >= (int)(w & 1u)) pos += 1;
+  return pos;
+}
+
 // Env-wide unit masks from the per-unit state just published (all threads).
 template <int W>
 __device__ __forceinline__ void build_masks(EnvSmem<W>& S, int i, bool valid, bool active,
@@ -488,7 +503,7 @@ __device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs,
 // positions.  R rows per chunk; SF floats per stage buffer.  Each chunk is
 // zero-filled with 16-byte stores, then only the visible (observer, other)
 // pairs are written -- enumerated straight from the N-bit visibility rows
-// (popc prefix over the chunk's rows + __fns), so every lane works on a
+// (popc prefix over the chunk's rows + nth_set_bit), so every lane works on a
 // visible pair and hidden pairs cost nothing beyond the zero fill.
 template <int W>
 __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* __restrict__ glob,
@@ -520,47 +535,66 @@ __device__ __noinline__ void emit_observations(float* __restrict__ obs, float* _
         const int rr = e / TABX_OWN_DIM, f = e - rr * TABX_OWN_DIM;
         row0[rr * D + f] = S.own[r0 + rr][f];
       }
-      // visible pairs, one row at a time: thread j owns column j, so only the
-      // (few) visible pairs of the row execute the block write
+      // visible pairs of the chunk's rows (vis excludes inactive rows/columns)
+      int total = 0;
       for (int rr = 0; rr < nr; ++rr) {
         const int r = r0 + rr;
-        const int j = tid;
-        if (j < N && j != r && bit_of(&S.vis[r * W], j)) {
-          const int kk = j - (j > r ? 1 : 0);
-          float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
-          const float4* oj = reinterpret_cast<const float4*>(S.own[j]);
-          const float4 o0 = oj[0], o1 = oj[1], o2 = oj[2], o3 = oj[3];
-          blk[0] = o0.x;
-          blk[1] = o0.y;
-          blk[2] = f32_quot(S.px[j] - S.px[r], fw, rw);
-          blk[3] = f32_quot(S.py[j] - S.py[r], fh, rh);
-          blk[4] = o1.x;
-          blk[5] = o1.y;
-          blk[6] = o1.z;
-          blk[7] = o1.w;
-          blk[8] = o2.x;
-          blk[9] = o2.y;
-          blk[10] = o2.z;
-          blk[11] = o2.w;
-          blk[12] = o3.x;
-          blk[13] = o3.y;
-          blk[14] = o3.z;
-          blk[15] = (S.uf[j] & UF_ENEMY) ? 1.0f : 0.0f;
-          blk[16] = bit_of(&S.atk[r * W], j) ? 1.0f : 0.0f;
-        }
-        // zone blocks of row r: thread z (stay zero for unused slots / inactive rows)
-        if (tid < Z && (S.uf[r] & UF_ACTIVE)) {
-          const int z = tid;
-          const int ty = C->zone_type[z];
-          if (ty != TABX_ZONE_NONE) {
-            float* zb = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
-            zb[ty - 1] = 1.0f;
-            zb[3] = f32_quot(C->zone_cx[z] - S.px[r], fw, rw);
-            zb[4] = f32_quot(C->zone_cy[z] - S.py[r], fh, rh);
-            zb[5] = __double2float_rn(C->zone_ax[z]);
-            zb[6] = __double2float_rn(C->zone_ay[z]);
-            zb[7] = __double2float_rn(C->zone_effect[z]);
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+          total += __popc(S.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u));
+      }
+      for (int s = tid; s < total; s += NT) {
+        int rr = 0, n = s, j = -1;
+        for (; rr < nr; ++rr) {
+          const int r = r0 + rr;
+          for (int k = 0; k < W && j < 0; ++k) {
+            const uint32_t w = S.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u);
+            const int c = __popc(w);
+            if (n < c) {
+              j = (k << 5) + nth_set_bit(w, n);
+            } else {
+              n -= c;
+            }
           }
+          if (j >= 0) break;
+        }
+        const int r = r0 + rr;
+        const int kk = j - (j > r ? 1 : 0);
+        float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
+        const float4* oj = reinterpret_cast<const float4*>(S.own[j]);
+        const float4 o0 = oj[0], o1 = oj[1], o2 = oj[2], o3 = oj[3];
+        blk[0] = o0.x;
+        blk[1] = o0.y;
+        blk[2] = f32_quot(S.px[j] - S.px[r], fw, rw);
+        blk[3] = f32_quot(S.py[j] - S.py[r], fh, rh);
+        blk[4] = o1.x;
+        blk[5] = o1.y;
+        blk[6] = o1.z;
+        blk[7] = o1.w;
+        blk[8] = o2.x;
+        blk[9] = o2.y;
+        blk[10] = o2.z;
+        blk[11] = o2.w;
+        blk[12] = o3.x;
+        blk[13] = o3.y;
+        blk[14] = o3.z;
+        blk[15] = (S.uf[j] & UF_ENEMY) ? 1.0f : 0.0f;
+        blk[16] = bit_of(&S.atk[r * W], j) ? 1.0f : 0.0f;
+      }
+      // zone blocks: thread z of each row (stay zero for unused slots / inactive rows)
+      if (tid < Z) {
+        const int z = tid;
+        const int ty = C->zone_type[z];
+        for (int rr = 0; rr < nr && ty != TABX_ZONE_NONE; ++rr) {
+          const int r = r0 + rr;
+          if (!(S.uf[r] & UF_ACTIVE)) continue;
+          float* zb = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
+          zb[ty - 1] = 1.0f;
+          zb[3] = f32_quot(C->zone_cx[z] - S.px[r], fw, rw);
+          zb[4] = f32_quot(C->zone_cy[z] - S.py[r], fh, rh);
+          zb[5] = __double2float_rn(C->zone_ax[z]);
+          zb[6] = __double2float_rn(C->zone_ay[z]);
+          zb[7] = __double2float_rn(C->zone_effect[z]);
         }
       }
       fence_proxy_async();
