@@ -709,7 +709,7 @@ __device__ __forceinline__ void team_ratios(EnvSmem<W>& S, int i, int N, bool ac
 // Heuristic opponent decision for unit i (heuristics.py:103-243).
 // Returns the action and updates the scripted-controller memory.
 template <int W>
-__device__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
+__device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
                                int N, int Z, const UnitStatic& U, const uint32_t (&vis)[W],
                                const uint32_t (&atk)[W], double hd, double cd, double step,
                                uint32_t mask7, double u_explore, double u_pick, double eps,
