@@ -12,6 +12,19 @@ cudaError_t launch_lanes_w1(const Params& P, int sm_count, cudaStream_t stream, 
 cudaError_t launch_lanes_w2(const Params& P, int sm_count, cudaStream_t stream, int* grid);
 cudaError_t launch_lanes_w4(const Params& P, int sm_count, cudaStream_t stream, int* grid);
 cudaError_t launch_lanes_w8(const Params& P, int sm_count, cudaStream_t stream, int* grid);
+cudaError_t launch_emit_w1(const Params& P, int sm_count, cudaStream_t stream);
+cudaError_t launch_emit_w2(const Params& P, int sm_count, cudaStream_t stream);
+cudaError_t launch_emit_w4(const Params& P, int sm_count, cudaStream_t stream);
+cudaError_t launch_emit_w8(const Params& P, int sm_count, cudaStream_t stream);
+
+cudaError_t launch_emit(const Params& P, int W, int sm_count, cudaStream_t stream) {
+  switch (W) {
+    case 1: return launch_emit_w1(P, sm_count, stream);
+    case 2: return launch_emit_w2(P, sm_count, stream);
+    case 4: return launch_emit_w4(P, sm_count, stream);
+    default: return launch_emit_w8(P, sm_count, stream);
+  }
+}
 
 // External action validation (environment.py:166-178): first offender in
 // row-major order is latched with atomicMin before any lane mutates.

@@ -12,6 +12,7 @@
 
 namespace tabx {
 cudaError_t launch_lanes(const Params& P, int W, int sm_count, cudaStream_t stream, int* grid);
+cudaError_t launch_emit(const Params& P, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
                             int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream);
 cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const DerivedCfg* dcfgs,
@@ -48,7 +49,6 @@ struct tabx_handle {
   Sync* sync = nullptr;
   double* stats_dev = nullptr;
   const int64_t* last_actions = nullptr;
-  int stage_bytes = 6144;  // observation staging bytes per buffer per env
 };
 
 static thread_local std::string g_err;
@@ -108,14 +108,6 @@ static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
   P.G = h->G;
   P.auto_reset = h->auto_reset;
   P.mode = mode;
-  // observation staging: R rows per chunk, two buffers per environment
-  const int budget = h->stage_bytes;
-  int R = budget / (4 * h->D);
-  if (R < 1) R = 1;
-  if (R > h->N) R = h->N;
-  int need = (R * h->D > h->G ? R * h->D : h->G) + 8;
-  P.stage_rows = R;
-  P.stage_floats = (need + 3) & ~3;
   return P;
 }
 
@@ -188,8 +180,6 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   h->D = tabx_obs_dim(N, Z);
   h->G = tabx_global_dim(N, Z);
   h->auto_reset = auto_reset ? 1 : 0;
-  h->stage_bytes = h->W == 1 ? 6144 : 16384;
-  if (const char* sb = getenv("TABX_STAGE_BYTES")) h->stage_bytes = atoi(sb);
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device);
 
   const int64_t B = batch, U = batch * N, W = h->W;
@@ -324,6 +314,7 @@ int tabx_init_output(tabx_handle* h, const tabx_outputs* out) {
   DeviceGuard guard(h->device);
   Params P = make_params(h, MODE_INIT, nullptr, out);
   TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "init_output launch");
+  TABX_CUDA(launch_emit(P, h->W, h->sm_count, h->stream), "emit launch");
   // fresh caches everywhere: nothing left to refresh
   TABX_CUDA(cudaMemsetAsync(h->sync->refresh, 0, sizeof(h->sync->refresh), h->stream),
             "refresh clear");
@@ -341,8 +332,12 @@ int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
               "validate launch");
   }
   h->last_actions = actions;
+  // K1 step logic -> K2 observation streaming -> K3 deferred auto-resets
   Params P = make_params(h, MODE_STEP, actions, out);
   TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "step launch");
+  TABX_CUDA(launch_emit(P, h->W, h->sm_count, h->stream), "emit launch");
+  P.mode = MODE_RESET;
+  TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "reset launch");
   return TABX_OK;
 }
 

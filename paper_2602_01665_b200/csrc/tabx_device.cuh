@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "../../include/tabx.h"
+#include <math.h>
 
 namespace tabx {
 
@@ -19,6 +20,7 @@ constexpr int TAG_RESEED = 2, TAG_EXPLORE = 3, TAG_PICK = 4, TAG_RANDOM = 5;
 
 // lane flag bits (DevState::flags)
 constexpr uint8_t F_DONE = 1, F_TERM = 2, F_TRUNC = 4;
+constexpr uint8_t F_PEND = 8;  // auto-reset pending (step kernel -> reset kernel)
 // unit bits (DevState::ubits)
 constexpr uint8_t U_ALIVE = 1, U_MEMV = 2;
 
@@ -80,7 +82,7 @@ struct DerivedCfg {
   int32_t n_ally, n_enemy;            // team roster sizes (active units)
 };
 
-enum Mode : int { MODE_STEP = 0, MODE_INIT = 1, MODE_REFRESH = 2 };
+enum Mode : int { MODE_STEP = 0, MODE_INIT = 1, MODE_REFRESH = 2, MODE_RESET = 3 };
 
 struct Params {
   DevState st;
@@ -93,8 +95,6 @@ struct Params {
   int N, Z, D, G;
   int auto_reset;
   int mode;
-  int stage_rows;    // observation rows per staged chunk
-  int stage_floats;  // floats per stage buffer (multiple of 4)
 };
 
 __device__ __noinline__ static bool zone_exact(double ex, double ey, double ax, double ay) {
@@ -130,4 +130,19 @@ __device__ __forceinline__ uint32_t zone_bits(const tabx_config* __restrict__ C,
   return bits;
 }
 
+// Rare exact fallbacks live out of line: a call cannot be speculated, so the
+// float64 division / square-root sequences only run on the lanes that need
+// them instead of being if-converted into every warp's path.
+static __device__ __noinline__ double slow_div(double x, double y) { return x / y; }
+static __device__ __noinline__ double slow_sqrt(double x) { return sqrt(x); }
+
+__device__ __forceinline__ float f32_quot(double x, double y, double ry) {
+  double q = x * ry;
+  const int dlt = (int)((uint32_t)__double2loint(q) & 0x1FFFFFFFu) - 0x10000000;
+  const double aq = fabs(q);
+  if ((dlt <= 8 && dlt >= -8) || (aq < 2.4e-38 && aq != 0.0) || aq > 1e37) q = slow_div(x, y);
+  return __double2float_rn(q);
+}
+
+// effective_speed multiplier: sequential product over zones (arrays.py:338-343)
 }  // namespace tabx

@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include "tabx_device.cuh"
+#include "tabx_emit.cuh"
 #include "tabx_math.cuh"
 
 namespace tabx {
@@ -52,7 +53,6 @@ struct EnvSmem {
   static constexpr int NT = 32 * W;
   double px[NT], py[NT], ch[NT], sh[NT], rad[NT], mh[NT], rv[NT], dmg[NT];
   double vx[NT], vy[NT], sx[NT], sy[NT];
-  float own[NT][16] __attribute__((aligned(16)));  // 15 own features + pad
   uint32_t vis[NT * W], atk[NT * W], touch[NT * W];
   uint32_t uf[NT];
   uint32_t zin[NT];
@@ -160,21 +160,6 @@ __device__ __forceinline__ bool bit_of(const uint32_t* row, int j) {
 // within 3 ulp of fl64(x / y), so both round to the same float32 unless q
 // sits within a few ulp of a float32 rounding midpoint (low 29 mantissa bits
 // near 0x10000000) -- then, and for float32-subnormal magnitudes, divide.
-// Rare exact fallbacks live out of line: a call cannot be speculated, so the
-// float64 division / square-root sequences only run on the lanes that need
-// them instead of being if-converted into every warp's path.
-static __device__ __noinline__ double slow_div(double x, double y) { return x / y; }
-static __device__ __noinline__ double slow_sqrt(double x) { return sqrt(x); }
-
-__device__ __forceinline__ float f32_quot(double x, double y, double ry) {
-  double q = x * ry;
-  const int dlt = (int)((uint32_t)__double2loint(q) & 0x1FFFFFFFu) - 0x10000000;
-  const double aq = fabs(q);
-  if ((dlt <= 8 && dlt >= -8) || (aq < 2.4e-38 && aq != 0.0) || aq > 1e37) q = slow_div(x, y);
-  return __double2float_rn(q);
-}
-
-// effective_speed multiplier: sequential product over zones (arrays.py:338-343)
 __device__ __forceinline__ double swamp_mult(const tabx_config* __restrict__ C, int Z,
                                              uint32_t zin, uint32_t swamp_m) {
   double m = 1.0;
@@ -450,223 +435,6 @@ __device__ __forceinline__ int cache_row_inl(EnvSmem<W>& S, int i, int N, const 
   return cache_row_body<W>(S, i, N, U.cos_half, U.srange, U.dmg, U.range, U.rad, bush_m);
 }
 
-// ------------------------------------------------ observation streaming --
-// Observation rows are assembled in shared memory (one thread per (observer,
-// other) pair block, one per own / zone block) and leave through TMA bulk
-// stores (cp.async.bulk.global.shared::cta), double-buffered so the fill of
-// chunk c+1 overlaps the store of chunk c.  The 16-byte aligned interior of
-// each chunk goes by TMA; the <= 3-float head and tail by plain stores.
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void bulk_s2g(void* g, const void* s, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g),
-               "r"(smem_addr(s)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() {
-  asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-}
-template <int K>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(K) : "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-
-// dst[gs, gs+count) <- stage[pad, pad+count), pad = gs & 3.
-template <int W>
-__device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs, int count,
-                                            const float* stage, int tid) {
-  constexpr int NT = 32 * W;
-  const int pad = (int)(gs & 3);
-  const int64_t a0 = (gs + 3) & ~(int64_t)3;
-  const int64_t a1 = (gs + count) & ~(int64_t)3;
-  if (a1 > a0) {
-    if (tid == 0) {
-      bulk_s2g(dst + a0, stage + pad + (a0 - gs), (uint32_t)((a1 - a0) * 4));
-      bulk_commit();
-    }
-    for (int e = tid; e < (int)(a0 - gs); e += NT) dst[gs + e] = stage[pad + e];
-    for (int e = (int)(a1 - gs) + tid; e < count; e += NT) dst[gs + e] = stage[pad + e];
-  } else {
-    for (int e = tid; e < count; e += NT) dst[gs + e] = stage[pad + e];
-  }
-}
-
-// Observation rows of one environment (perception.py:159-192) and its
-// global-state row (perception.py:194-200), from S.own / S.vis / S.atk /
-// positions.  R rows per chunk; SF floats per stage buffer.  Each chunk is
-// zero-filled with 16-byte stores, then only the visible (observer, other)
-// pairs are written -- enumerated straight from the N-bit visibility rows
-// (popc prefix over the chunk's rows + nth_set_bit), so every lane works on a
-// visible pair and hidden pairs cost nothing beyond the zero fill.
-template <int W>
-__device__ __noinline__ void emit_observations(float* __restrict__ obs, float* __restrict__ glob,
-                                               int64_t b, int N, int Z, int D, int G, int R,
-                                               int SF, EnvSmem<W>& S, float* stage,
-                                               const tabx_config* __restrict__ C,
-                                               const DerivedCfg* __restrict__ DC, int tid) {
-  constexpr int NT = 32 * W;
-  const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
-  const int M = N - 1;
-  const int zoff = TABX_OWN_DIM + TABX_OTHER_DIM * M;
-  int buf = 0;
-  if (obs) {
-    for (int r0 = 0; r0 < N; r0 += R) {
-      const int nr = min(R, N - r0);
-      const int64_t gs = (b * N + r0) * (int64_t)D;
-      float* st = stage + buf * SF;
-      const int pad = (int)(gs & 3);
-      float* row0 = st + pad;
-      if (tid == 0) bulk_wait_read<1>();
-      env_sync<W>();
-      {
-        const int n4 = (pad + nr * D + 3) >> 2;
-        float4* z4 = reinterpret_cast<float4*>(st);
-        for (int q = tid; q < n4; q += NT) z4[q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      }
-      env_sync<W>();
-      for (int e = tid; e < nr * TABX_OWN_DIM; e += NT) {
-        const int rr = e / TABX_OWN_DIM, f = e - rr * TABX_OWN_DIM;
-        row0[rr * D + f] = S.own[r0 + rr][f];
-      }
-      // visible pairs of the chunk's rows (vis excludes inactive rows/columns)
-      int total = 0;
-      for (int rr = 0; rr < nr; ++rr) {
-        const int r = r0 + rr;
-#pragma unroll
-        for (int k = 0; k < W; ++k)
-          total += __popc(S.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u));
-      }
-      for (int s = tid; s < total; s += NT) {
-        int rr = 0, n = s, j = -1;
-        for (; rr < nr; ++rr) {
-          const int r = r0 + rr;
-          for (int k = 0; k < W && j < 0; ++k) {
-            const uint32_t w = S.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u);
-            const int c = __popc(w);
-            if (n < c) {
-              j = (k << 5) + nth_set_bit(w, n);
-            } else {
-              n -= c;
-            }
-          }
-          if (j >= 0) break;
-        }
-        const int r = r0 + rr;
-        const int kk = j - (j > r ? 1 : 0);
-        float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
-        const float4* oj = reinterpret_cast<const float4*>(S.own[j]);
-        const float4 o0 = oj[0], o1 = oj[1], o2 = oj[2], o3 = oj[3];
-        blk[0] = o0.x;
-        blk[1] = o0.y;
-        blk[2] = f32_quot(S.px[j] - S.px[r], fw, rw);
-        blk[3] = f32_quot(S.py[j] - S.py[r], fh, rh);
-        blk[4] = o1.x;
-        blk[5] = o1.y;
-        blk[6] = o1.z;
-        blk[7] = o1.w;
-        blk[8] = o2.x;
-        blk[9] = o2.y;
-        blk[10] = o2.z;
-        blk[11] = o2.w;
-        blk[12] = o3.x;
-        blk[13] = o3.y;
-        blk[14] = o3.z;
-        blk[15] = (S.uf[j] & UF_ENEMY) ? 1.0f : 0.0f;
-        blk[16] = bit_of(&S.atk[r * W], j) ? 1.0f : 0.0f;
-      }
-      // zone blocks: thread z of each row (stay zero for unused slots / inactive rows)
-      if (tid < Z) {
-        const int z = tid;
-        const int ty = C->zone_type[z];
-        for (int rr = 0; rr < nr && ty != TABX_ZONE_NONE; ++rr) {
-          const int r = r0 + rr;
-          if (!(S.uf[r] & UF_ACTIVE)) continue;
-          float* zb = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
-          zb[ty - 1] = 1.0f;
-          zb[3] = f32_quot(C->zone_cx[z] - S.px[r], fw, rw);
-          zb[4] = f32_quot(C->zone_cy[z] - S.py[r], fh, rh);
-          zb[5] = __double2float_rn(C->zone_ax[z]);
-          zb[6] = __double2float_rn(C->zone_ay[z]);
-          zb[7] = __double2float_rn(C->zone_effect[z]);
-        }
-      }
-      fence_proxy_async();
-      env_sync<W>();
-      flush_stage<W>(obs, gs, nr * D, st, tid);
-      buf ^= 1;
-    }
-  }
-  if (glob) {
-    const int64_t gs = b * (int64_t)G;
-    float* st = stage + buf * SF;
-    float* row = st + (int)(gs & 3);
-    if (tid == 0) bulk_wait_read<1>();
-    env_sync<W>();
-    for (int e = tid; e < N * TABX_OWN_DIM; e += NT) {
-      const int u = e / TABX_OWN_DIM;
-      row[e] = S.own[u][e - u * TABX_OWN_DIM];
-    }
-    for (int q = tid; q < Z * TABX_ZONE_DIM; q += NT) {
-      const int z = q >> 3, f = q & 7;
-      const int ty = C->zone_type[z];
-      float v;
-      if (ty == TABX_ZONE_NONE) {
-        v = 0.0f;
-      } else {
-        switch (f) {
-          case 0: case 1: case 2: v = ty == f + 1 ? 1.0f : 0.0f; break;
-          case 3: v = f32_quot(C->zone_cx[z], fw, rw); break;
-          case 4: v = f32_quot(C->zone_cy[z], fh, rh); break;
-          case 5: v = __double2float_rn(C->zone_ax[z]); break;
-          case 6: v = __double2float_rn(C->zone_ay[z]); break;
-          default: v = __double2float_rn(C->zone_effect[z]); break;
-        }
-      }
-      row[N * TABX_OWN_DIM + q] = v;
-    }
-    fence_proxy_async();
-    env_sync<W>();
-    flush_stage<W>(glob, gs, G, st, tid);
-  }
-  if (tid == 0) bulk_wait_read<0>();
-  env_sync<W>();
-}
-
-// Own-feature block of unit i (perception.py:108-132) rounded to float32.
-__device__ __forceinline__ void own_features(float* o, const UnitStatic& U, double rmh,
-                                             double rucd, double hp, double px, double py,
-                                             double ch, double sh, double cd, bool alive,
-                                             double fw, double fh, double rw, double rh) {
-  o[15] = 0.0f;
-  if (!U.active) {
-#pragma unroll
-    for (int f = 0; f < TABX_OWN_DIM; ++f) o[f] = 0.0f;
-    return;
-  }
-  o[0] = f32_quot(hp, U.mh, rmh);
-  o[1] = f32_quot(U.mh, 1000.0, 0.001);
-  o[2] = f32_quot(px, fw, rw);
-  o[3] = f32_quot(py, fh, rh);
-  o[4] = __double2float_rn(ch);
-  o[5] = __double2float_rn(sh);
-  o[6] = __double2float_rn(U.range);
-  o[7] = __double2float_rn(U.dmg);
-  o[8] = __double2float_rn(cd);
-  o[9] = U.ucd > 0.0 ? f32_quot(cd, U.ucd, rucd) : 0.0f;
-  o[10] = __double2float_rn(U.rad);
-  o[11] = __double2float_rn(U.mass);
-  o[12] = __double2float_rn(U.sangle);
-  o[13] = alive ? 1.0f : 0.0f;
-  o[14] = __double2float_rn(U.speed);
-}
-
 // Team health ratio sums in numpy pairwise order (arrays.py:390-400); one
 // thread, values staged in S.vx (ally) / S.vy (enemy).
 template <int W>
@@ -817,7 +585,7 @@ __device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_conf
 // ---------------------------------------------------------------- lane ---
 template <int W>
 __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
-                         float* stage, bool refresh, uint32_t step_no) {
+                         EmitEnv<W>* emit, bool refresh, uint32_t step_no) {
   const int N = P.N, Z = P.Z;
   const bool valid = i < N;
   const int64_t u = b * N + i;
@@ -888,6 +656,90 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   uint32_t vis[W], atk[W];
   int tgt = -1;
 
+  if (P.mode == MODE_RESET) {
+    // deferred auto-reset of a finished lane (environment.py:502-517): reseed,
+    // respawn from the config template, fresh caches and prev_gap, then the
+    // fresh observation / mask replace the step's (final ones were written by
+    // the emit kernel)
+    if (!(lf & F_PEND)) return;
+    const int64_t episode = st.episode[b] + 1;
+    seed = key_hash(seed, (uint64_t)episode, TAG_RESEED, 0);
+    if (valid && U.active) {
+      px = C->spawn_x[i];
+      py = C->spawn_y[i];
+      hd = C->spawn_heading[i];
+      hp = U.mh;
+      alive = true;
+    } else {
+      alive = false;
+    }
+    ivx = ivy = vlx = vly = 0.0;
+    cd = rv = 0.0;
+    mx = my = 0.0;
+    memv = false;
+    t = 0;
+    ep_ret = 0.0;
+    lf = 0;
+    winner = -1;
+    reason = R_NONE;
+    fk = -1;
+    ch = libm_cos(hd);
+    sh = libm_sin(hd);
+    zin = valid ? zone_bits(C, DC, Z, px, py) : 0u;
+    publish();
+    build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
+    env_sync<W>();
+    cache_row_of<W>(S, i, N, U, bush_m);
+    double ra, re;
+    team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
+    prev_gap = ra - re;
+    const tabx_outputs& O = P.out;
+    if (valid) {
+      st.pos[u] = make_double2(px, py);
+      st.heading[u] = hd;
+      st.vel[u] = make_double2(0.0, 0.0);
+      st.imp_dv[u] = make_double2(0.0, 0.0);
+      st.health[u] = hp;
+      st.cooldown[u] = 0.0;
+      st.reveal[u] = 0.0;
+      st.mem_pos[u] = make_double2(0.0, 0.0);
+      st.hcs[u] = make_double2(ch, sh);
+      st.zbits[u] = zin;
+      st.ubits[u] = alive ? U_ALIVE : 0;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        st.vis[u * W + k] = S.vis[i * W + k];
+        st.atk[u * W + k] = S.atk[i * W + k];
+      }
+      if (O.action_mask) {
+        const bool c2 = alive && U.active;
+        uint8_t* m = O.action_mask + u * TABX_NUM_ACTIONS;
+        for (int a = 0; a < 5; ++a) m[a] = c2;
+        m[5] = c2;
+        m[6] = (c2 && C->enable_noop) || !c2;
+      }
+    }
+    if (i == 0) {
+      st.episode[b] = episode;
+      st.seed[b] = seed;
+      st.t[b] = 0;
+      st.prev_gap[b] = prev_gap;
+      st.ep_return[b] = 0.0;
+      st.flags[b] = 0;
+      st.winner[b] = -1;
+      st.reason[b] = R_NONE;
+      st.first_kill[b] = -1;
+      P.sync->refresh[(step_no + 1) % 3] = 1;
+    }
+    env_sync<W>();
+    if (emit && i < 32) {
+      load_view<W>(*emit, st, b, N, C, DC, i);
+      emit_lane<W>(*emit, O.observations, O.global_state, b, N, Z, P.D, P.G, C, DC, i);
+    }
+    env_sync<W>();
+    return;
+  }
+
   if (P.mode != MODE_STEP) {
     // init_output / refresh_caches (environment.py:147-151, :351-374)
     publish();
@@ -915,11 +767,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     double ra, re;
     team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
     prev_gap = ra - re;
-    own_features(S.own[i], U, rmh, rucd, hp, px, py, ch, sh, cd, alive, fw, fh, rw, rh);
-    env_sync<W>();
     const tabx_outputs& O = P.out;
-    emit_observations<W>(O.observations, O.global_state, b, N, Z, P.D, P.G, P.stage_rows,
-                         P.stage_floats, S, stage, C, DC, i);
     if (valid) {
       const bool ctl = alive && U.active;
       if (O.action_mask) {
@@ -1213,15 +1061,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   // ---- outputs of this step (observation uses stage-8 caches, post-step state)
   const tabx_outputs& O = P.out;
   const bool resets = P.auto_reset && (lf & F_DONE);
-  own_features(S.own[i], U, rmh, rucd, hp, px, py, ch, sh, cd, alive, fw, fh, rw, rh);
-  S.uf[i] = (S.uf[i] & ~UF_ALIVE) | (alive ? UF_ALIVE : 0u);
-  env_sync<W>();
-  {
-    float* ob = resets ? O.final_observations : O.observations;
-    float* gb = resets ? O.final_global_state : O.global_state;
-    emit_observations<W>(ob, gb, b, N, Z, P.D, P.G, P.stage_rows, P.stage_floats, S, stage, C,
-                         DC, i);
-  }
+  if (resets) lf |= F_PEND;  // the reset kernel respawns after the emit kernel
   if (valid) {
     if (O.rewards) O.rewards[u] = (float)reward_i;
     if (O.actions) O.actions[u] = act;
@@ -1254,62 +1094,6 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
       st.st_elims[b] += elim ? 1 : 0;
       st.st_len[b] += t;
       st.st_ret[b] += ep_ret;
-    }
-  }
-
-  if (resets) {
-    // auto-reset (environment.py:502-517): reseed, respawn, fresh caches
-    env_sync<W>();
-    const int64_t episode = st.episode[b] + 1;
-    seed = key_hash(seed, (uint64_t)episode, TAG_RESEED, 0);
-    if (valid && U.active) {
-      px = C->spawn_x[i];
-      py = C->spawn_y[i];
-      hd = C->spawn_heading[i];
-      hp = U.mh;
-      alive = true;
-    } else {
-      alive = false;
-    }
-    ivx = ivy = vlx = vly = 0.0;
-    cd = rv = 0.0;
-    mx = my = 0.0;
-    memv = false;
-    t = 0;
-    ep_ret = 0.0;
-    lf = 0;
-    winner = -1;
-    reason = R_NONE;
-    fk = -1;
-    ch = libm_cos(hd);
-    sh = libm_sin(hd);
-    zin = valid ? zone_bits(C, DC, Z, px, py) : 0u;
-    publish();
-    build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
-    env_sync<W>();
-    cache_row_of<W>(S, i, N, U, bush_m);
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      vis[k] = S.vis[i * W + k];
-      atk[k] = S.atk[i * W + k];
-    }
-    team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
-    prev_gap = ra - re;
-    own_features(S.own[i], U, rmh, rucd, hp, px, py, ch, sh, cd, alive, fw, fh, rw, rh);
-    env_sync<W>();
-    emit_observations<W>(O.observations, O.global_state, b, N, Z, P.D, P.G, P.stage_rows,
-                         P.stage_floats, S, stage, C, DC, i);
-    if (valid && O.action_mask) {
-      const bool c2 = alive && U.active;
-      uint8_t* m = O.action_mask + u * TABX_NUM_ACTIONS;
-      for (int a = 0; a < 5; ++a) m[a] = c2;
-      m[5] = c2 && cd <= 0.0;
-      m[6] = (c2 && C->enable_noop) || !c2;
-    }
-    if (i == 0) {
-      st.episode[b] = episode;
-      st.seed[b] = seed;
-      P.sync->refresh[(step_no + 1) % 3] = 1;
     }
   }
 
@@ -1347,32 +1131,37 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 #ifndef TABX_MIN_BLOCKS
 #define TABX_MIN_BLOCKS 3
 #endif
+// K1 (MODE_STEP / MODE_INIT / MODE_REFRESH) and K3 (MODE_RESET).
 template <int W, int EPB>
 __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
     lane_kernel(const Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EnvSmem<W>* envs = reinterpret_cast<EnvSmem<W>*>(smem_raw);
   const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
-  float* stages = reinterpret_cast<float*>(smem_raw + env_bytes);
+  EmitEnv<W>* views =
+      P.mode == MODE_RESET ? reinterpret_cast<EmitEnv<W>*>(smem_raw + env_bytes) : nullptr;
 
   uint32_t step_no = 0;
   bool refresh = false;
-  if (P.mode == MODE_STEP) {
+  if (P.mode == MODE_STEP || P.mode == MODE_RESET) {
     if (P.sync->err_index != NO_ERROR) return;  // an action violated the mask: no mutation
     step_no = P.sync->step;
     refresh = P.sync->refresh[step_no % 3] != 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.sync->refresh[(step_no + 2) % 3] = 0;
+    if (P.mode == MODE_STEP && blockIdx.x == 0 && threadIdx.x == 0)
+      P.sync->refresh[(step_no + 2) % 3] = 0;
   } else if (P.mode == MODE_REFRESH) {
     step_no = P.sync->step;
     refresh = P.sync->refresh[step_no % 3] != 0;
   }
   const int g = threadIdx.x / (32 * W);
   const int i = threadIdx.x % (32 * W);
-  for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB)
-    run_lane<W>(P, b, i, envs[g], stages + (size_t)g * 2 * P.stage_floats, refresh, step_no);
-  if (i == 0) bulk_wait_all();  // bulk stores issued by this thread are complete
+  for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB) {
+    if (P.mode == MODE_RESET && !(P.st.flags[b] & F_PEND)) continue;  // env-uniform
+    run_lane<W>(P, b, i, envs[g], views ? views + g : nullptr, refresh, step_no);
+  }
 
-  if (P.mode == MODE_STEP) {
+  if (P.mode == MODE_RESET) {
+    // the reset kernel ends the step: advance the device step counter
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
@@ -1388,25 +1177,25 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
 
 // ------------------------------------------------------------ launchers --
 template <int W, int EPB>
-cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream,
-                                  int* grid_out) {
+cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream, int* grid_out) {
   const int threads = 32 * W * EPB;
   const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
-  const size_t smem = env_bytes + (size_t)EPB * 2 * P.stage_floats * sizeof(float);
+  const size_t smem = env_bytes + (P.mode == MODE_RESET ? sizeof(EmitEnv<W>) * EPB : 0);
   // attribute + occupancy are host-side queries; cache them per smem size so a
-  // step costs one launch (and stays capturable in a CUDA graph)
-  static size_t cached_smem = 0;
-  static int cached_per_sm = 0;
-  int per_sm = cached_per_sm;
-  if (smem != cached_smem) {
+  // step costs one launch per kernel (and stays capturable in a CUDA graph)
+  static size_t cached_smem[2] = {0, 0};
+  static int cached_per_sm[2] = {0, 0};
+  const int slot = P.mode == MODE_RESET ? 1 : 0;
+  int per_sm = cached_per_sm[slot];
+  if (smem != cached_smem[slot]) {
     cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lane_kernel<W, EPB>, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
-    cached_smem = smem;
-    cached_per_sm = per_sm;
+    cached_smem[slot] = smem;
+    cached_per_sm[slot] = per_sm;
   }
   int64_t need = (P.B + EPB - 1) / EPB;
   int64_t cap = (int64_t)sm_count * per_sm;

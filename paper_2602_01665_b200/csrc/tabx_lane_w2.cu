@@ -1,8 +1,11 @@
-// Lane-kernel instantiation for W = 2 (64 threads per environment).
+// Kernel instantiations for W = 2 (64 threads per environment).
 #include "tabx_lane.cuh"
 
 namespace tabx {
 cudaError_t launch_lanes_w2(const Params& P, int sm_count, cudaStream_t stream, int* grid) {
   return launch_lanes_t<2, 1>(P, sm_count, stream, grid);
+}
+cudaError_t launch_emit_w2(const Params& P, int sm_count, cudaStream_t stream) {
+  return launch_emit_t<2, 4>(P, sm_count, stream);
 }
 }  // namespace tabx
