@@ -109,21 +109,6 @@ __device__ __forceinline__ int env_count(bool p, EnvSmem<W>& S, int i) {
   return c;
 }
 
-// Position of the n-th (0-based) set bit of w, by popc halving.
-__device__ __forceinline__ int nth_set_bit(uint32_t w, int n) {
-  int pos = 0;
-  int c = __popc(w & 0xFFFFu);
-  if (n >= c) { n -= c; w >>= 16; pos += 16; }
-  c = __popc(w & 0xFFu);
-  if (n >= c) { n -= c; w >>= 8; pos += 8; }
-  c = __popc(w & 0xFu);
-  if (n >= c) { n -= c; w >>= 4; pos += 4; }
-  c = __popc(w & 0x3u);
-  if (n >= c) { n -= c; w >>= 2; pos += 2; }
-  if (n >= (int)(w & 1u)) pos += 1;
-  return pos;
-}
-
 // Env-wide unit masks from the per-unit state just published (all threads).
 template <int W>
 __device__ __forceinline__ void build_masks(EnvSmem<W>& S, int i, bool valid, bool active,
@@ -733,8 +718,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     }
     env_sync<W>();
     if (emit && i < 32) {
+      const int R = emit_rows(N, P.D, W == 1 ? 3200 : 8192);
+      const int SF = emit_stage_floats(N, P.D, P.G, R);
+      float* stage = reinterpret_cast<float*>(emit + 1);
       load_view<W>(*emit, st, b, N, C, DC, i);
-      emit_lane<W>(*emit, O.observations, O.global_state, b, N, Z, P.D, P.G, C, DC, i);
+      emit_lane<W>(*emit, O.observations, O.global_state, b, N, Z, P.D, P.G, R, SF, stage, C, DC,
+                   i);
     }
     env_sync<W>();
     return;
@@ -1128,6 +1117,14 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   env_sync<W>();
 }
 
+// Per-env shared memory of the reset kernel's emitter: view + 2 stage buffers.
+template <int W>
+__host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
+  const int R = emit_rows(P.N, P.D, W == 1 ? 3200 : 8192);
+  const int SF = emit_stage_floats(P.N, P.D, P.G, R);
+  return ((sizeof(EmitEnv<W>) + 15) & ~(size_t)15) + (size_t)2 * SF * sizeof(float);
+}
+
 #ifndef TABX_MIN_BLOCKS
 #define TABX_MIN_BLOCKS 3
 #endif
@@ -1138,8 +1135,8 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EnvSmem<W>* envs = reinterpret_cast<EnvSmem<W>*>(smem_raw);
   const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
-  EmitEnv<W>* views =
-      P.mode == MODE_RESET ? reinterpret_cast<EmitEnv<W>*>(smem_raw + env_bytes) : nullptr;
+  const size_t view_bytes = reset_view_bytes<W>(P);
+  unsigned char* view_base = smem_raw + env_bytes;
 
   uint32_t step_no = 0;
   bool refresh = false;
@@ -1157,7 +1154,10 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
   const int i = threadIdx.x % (32 * W);
   for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB) {
     if (P.mode == MODE_RESET && !(P.st.flags[b] & F_PEND)) continue;  // env-uniform
-    run_lane<W>(P, b, i, envs[g], views ? views + g : nullptr, refresh, step_no);
+    run_lane<W>(P, b, i, envs[g],
+                P.mode == MODE_RESET ? reinterpret_cast<EmitEnv<W>*>(view_base + g * view_bytes)
+                                     : nullptr,
+                refresh, step_no);
   }
 
   if (P.mode == MODE_RESET) {
@@ -1180,7 +1180,7 @@ template <int W, int EPB>
 cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream, int* grid_out) {
   const int threads = 32 * W * EPB;
   const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
-  const size_t smem = env_bytes + (P.mode == MODE_RESET ? sizeof(EmitEnv<W>) * EPB : 0);
+  const size_t smem = env_bytes + (P.mode == MODE_RESET ? reset_view_bytes<W>(P) * EPB : 0);
   // attribute + occupancy are host-side queries; cache them per smem size so a
   // step costs one launch per kernel (and stays capturable in a CUDA graph)
   static size_t cached_smem[2] = {0, 0};
