@@ -294,8 +294,12 @@ __host__ __device__ __forceinline__ int emit_stage_floats(int N, int D, int G, i
 // whose auto-reset is pending: their terminal observation) or after
 // init_output.  EPW environments per CTA, one warp each; dynamic shared
 // memory = EPW x (view + 2 stage buffers of SF floats).
+#ifndef TABX_EMIT_MIN_BLOCKS
+#define TABX_EMIT_MIN_BLOCKS 3
+#endif
 template <int W, int EPW>
-__global__ void __launch_bounds__(32 * EPW) emit_kernel(const Params P, int R, int SF) {
+__global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS)
+    emit_kernel(const Params P, int R, int SF) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EmitEnv<W>* views = reinterpret_cast<EmitEnv<W>*>(smem_raw);
   float* stages = reinterpret_cast<float*>(smem_raw + ((sizeof(EmitEnv<W>) * EPW + 15) & ~15));
