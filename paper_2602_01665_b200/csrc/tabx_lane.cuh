@@ -1126,7 +1126,7 @@ __host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
 }
 
 #ifndef TABX_MIN_BLOCKS
-#define TABX_MIN_BLOCKS 3
+#define TABX_MIN_BLOCKS 4
 #endif
 // K1 (MODE_STEP / MODE_INIT / MODE_REFRESH) and K3 (MODE_RESET).
 template <int W, int EPB>
