@@ -10,16 +10,16 @@ import sys
 from collections import defaultdict
 
 
-def line_map(listing):
+def line_map(listing, fn="lane_kernel"):
     cur = None
     m = {}
     rx_line = re.compile(r'//## File "([^"]+)", line (\d+)')
     rx_ins = re.compile(r"/\*([0-9a-f]{4,})\*/")
     in_fn = False
     for raw in open(listing):
-        if ".text._ZN4tabx11lane_kernel" in raw and "section" in raw:
+        if ".text._ZN4tabx" in raw and fn in raw and "section" in raw:
             in_fn = True
-        elif raw.startswith("\t.section") and in_fn and "lane_kernel" not in raw:
+        elif raw.startswith("\t.section") and in_fn and fn not in raw:
             in_fn = False
         if not in_fn:
             continue
