@@ -25,7 +25,6 @@ struct EmitEnv {
   float own[NT][16] __attribute__((aligned(16)));
   uint32_t vis[NT * W], atk[NT * W];
   uint32_t flags[NT];  // bit0 active, bit1 enemy
-  int32_t pref[NT + 1];  // visible-pair prefix over a chunk's rows
 };
 
 __device__ __forceinline__ bool row_bit(const uint32_t* row, int j) {
@@ -64,22 +63,11 @@ __device__ __forceinline__ void own_from_state(float* o, const DevState& st, int
 }
 
 // Load lane b's view into E (all 32 lanes of the warp).
-template <int W, int TS>
-__device__ __forceinline__ void team_sync() {
-  if (TS == 32) {
-    __syncwarp();
-  } else {
-    __syncthreads();
-  }
-}
-
-// Load lane b's view into E (a team of TS threads; TS == 32: one warp,
-// otherwise the whole CTA).
-template <int W, int TS>
+template <int W>
 __device__ __forceinline__ void load_view(EmitEnv<W>& E, const DevState& st, int64_t b, int N,
                                           const tabx_config* __restrict__ C,
                                           const DerivedCfg* __restrict__ DC, int lane) {
-  for (int u = lane; u < N; u += TS) {
+  for (int u = lane; u < N; u += 32) {
     const int64_t gu = b * N + u;
     const double2 p = st.pos[gu];
     E.px[u] = p.x;
@@ -92,7 +80,7 @@ __device__ __forceinline__ void load_view(EmitEnv<W>& E, const DevState& st, int
       E.atk[u * W + k] = st.atk[gu * W + k];
     }
   }
-  team_sync<W, TS>();
+  __syncwarp();
 }
 
 // ---- TMA bulk stores (cp.async.bulk.global.shared::cta)
@@ -121,7 +109,6 @@ __device__ __forceinline__ void fence_proxy_async() {
 // dst[gs, gs+count) <- stage[pad, pad+count), pad = gs & 3: the 16-byte
 // aligned interior by one TMA bulk store (lane 0), the <= 3-float head and
 // tail by plain stores.
-template <int TS>
 __device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs, int count,
                                             const float* stage, int lane) {
   const int pad = (int)(gs & 3);
@@ -132,10 +119,10 @@ __device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs,
       bulk_s2g(dst + a0, stage + pad + (a0 - gs), (uint32_t)((a1 - a0) * 4));
       bulk_commit();
     }
-    for (int e = lane; e < (int)(a0 - gs); e += TS) dst[gs + e] = stage[pad + e];
-    for (int e = (int)(a1 - gs) + lane; e < count; e += TS) dst[gs + e] = stage[pad + e];
+    for (int e = lane; e < (int)(a0 - gs); e += 32) dst[gs + e] = stage[pad + e];
+    for (int e = (int)(a1 - gs) + lane; e < count; e += 32) dst[gs + e] = stage[pad + e];
   } else {
-    for (int e = lane; e < count; e += TS) dst[gs + e] = stage[pad + e];
+    for (int e = lane; e < count; e += 32) dst[gs + e] = stage[pad + e];
   }
 }
 
@@ -154,76 +141,63 @@ __device__ __forceinline__ int nth_bit(uint32_t w, int n) {
   return pos;
 }
 
-// Env b's observation rows and global-state row, built by a team of TS
-// threads.  Rows are assembled in shared memory R at a time: a 16-byte zero
-// fill, the own block, the visible (observer, other) pair blocks -- enumerated
-// from the N-bit visibility rows through a per-chunk prefix, so every thread
-// writes a visible pair -- and the zone blocks; each chunk then leaves through
-// one TMA bulk store (thread 0) while the team moves on.  Hidden pairs, most
-// of the tensor, cost only the fill.  `stage` holds SF floats, `gstage` G+8.
-template <int W, int TS>
-__device__ void emit_env(EmitEnv<W>& E, float* __restrict__ obs, float* __restrict__ glob,
-                         int64_t b, int N, int Z, int D, int G, int R, float* stage,
-                         float* gstage, const tabx_config* __restrict__ C,
-                         const DerivedCfg* __restrict__ DC, int t) {
+// Env b's observation rows and global-state row, one warp.  Rows are built
+// in shared memory R at a time (zero fill with 16-byte stores, then the own
+// block, the visible (observer, other) pair blocks enumerated from the N-bit
+// visibility rows, and the zone blocks) and leave through double-buffered
+// TMA bulk stores; hidden pairs -- most of the tensor -- cost only the fill.
+template <int W>
+__device__ void emit_lane(const EmitEnv<W>& E, float* __restrict__ obs, float* __restrict__ glob,
+                          int64_t b, int N, int Z, int D, int G, int R, int SF, float* stage,
+                          const tabx_config* __restrict__ C, const DerivedCfg* __restrict__ DC,
+                          int lane) {
   const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
   const int M = N - 1;
   const int zoff = TABX_OWN_DIM + TABX_OTHER_DIM * M;
+  int buf = 0;
   if (obs) {
     for (int r0 = 0; r0 < N; r0 += R) {
       const int nr = min(R, N - r0);
       const int64_t gs = (b * N + r0) * (int64_t)D;
+      float* st = stage + buf * SF;
       const int pad = (int)(gs & 3);
-      float* row0 = stage + pad;
-      if (t == 0) {
-        bulk_wait_read<0>();  // the previous chunk's TMA store has read the stage
-        int acc = 0;
-        E.pref[0] = 0;
-        for (int rr = 0; rr < nr; ++rr) {
-          const int r = r0 + rr;
-#pragma unroll
-          for (int k = 0; k < W; ++k)
-            acc += __popc(E.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u));
-          E.pref[rr + 1] = acc;
-        }
-      }
-      team_sync<W, TS>();
+      float* row0 = st + pad;
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
       {
         const int n4 = (pad + nr * D + 3) >> 2;
-        float4* z4 = reinterpret_cast<float4*>(stage);
-        const float4 zero = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        int q = t;
-        for (; q + 3 * TS < n4; q += 4 * TS) {
-          z4[q] = zero;
-          z4[q + TS] = zero;
-          z4[q + 2 * TS] = zero;
-          z4[q + 3 * TS] = zero;
-        }
-        for (; q < n4; q += TS) z4[q] = zero;
+        float4* z4 = reinterpret_cast<float4*>(st);
+        for (int q = lane; q < n4; q += 32) z4[q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
       }
-      team_sync<W, TS>();
-      for (int e = t; e < nr * TABX_OWN_DIM; e += TS) {
+      __syncwarp();
+      for (int e = lane; e < nr * TABX_OWN_DIM; e += 32) {
         const int rr = e / TABX_OWN_DIM, f = e - rr * TABX_OWN_DIM;
         row0[rr * D + f] = E.own[r0 + rr][f];
       }
-      const int total = E.pref[nr];
-      for (int s = t; s < total; s += TS) {
-        // row: largest rr with pref[rr] <= s (binary search over nr+1 entries)
-        int lo = 0, hi = nr;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (E.pref[mid] <= s) lo = mid; else hi = mid;
-        }
-        const int rr = lo;
+      // visible pairs of the chunk's rows (vis excludes inactive rows/columns)
+      int total = 0;
+      for (int rr = 0; rr < nr; ++rr) {
         const int r = r0 + rr;
-        int n = s - E.pref[rr], j = 0;
 #pragma unroll
-        for (int k = 0; k < W; ++k) {
-          const uint32_t w = E.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u);
-          const int c = __popc(w);
-          if (n >= 0 && n < c) j = (k << 5) + nth_bit(w, n);
-          n -= c;
+        for (int k = 0; k < W; ++k)
+          total += __popc(E.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u));
+      }
+      for (int s = lane; s < total; s += 32) {
+        int rr = 0, n = s, j = -1;
+        for (; rr < nr; ++rr) {
+          const int r = r0 + rr;
+          for (int k = 0; k < W && j < 0; ++k) {
+            const uint32_t w = E.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u);
+            const int c = __popc(w);
+            if (n < c) {
+              j = (k << 5) + nth_bit(w, n);
+            } else {
+              n -= c;
+            }
+          }
+          if (j >= 0) break;
         }
+        const int r = r0 + rr;
         const int kk = j - (j > r ? 1 : 0);
         float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
         const float4* oj = reinterpret_cast<const float4*>(E.own[j]);
@@ -246,35 +220,39 @@ __device__ void emit_env(EmitEnv<W>& E, float* __restrict__ obs, float* __restri
         blk[15] = (E.flags[j] & 2u) ? 1.0f : 0.0f;
         blk[16] = row_bit(&E.atk[r * W], j) ? 1.0f : 0.0f;
       }
-      // zone blocks of active rows (unused slots stay zero)
-      for (int q = t; q < nr * Z; q += TS) {
-        const int rr = q / Z, z = q - rr * Z;
-        const int r = r0 + rr;
+      // zone blocks: lane z of each active row (unused slots stay zero)
+      if (lane < Z) {
+        const int z = lane;
         const int ty = C->zone_type[z];
-        if (ty == TABX_ZONE_NONE || !(E.flags[r] & 1u)) continue;
-        float* zb = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
-        zb[ty - 1] = 1.0f;
-        zb[3] = f32_quot(C->zone_cx[z] - E.px[r], fw, rw);
-        zb[4] = f32_quot(C->zone_cy[z] - E.py[r], fh, rh);
-        zb[5] = __double2float_rn(C->zone_ax[z]);
-        zb[6] = __double2float_rn(C->zone_ay[z]);
-        zb[7] = __double2float_rn(C->zone_effect[z]);
+        for (int rr = 0; rr < nr && ty != TABX_ZONE_NONE; ++rr) {
+          const int r = r0 + rr;
+          if (!(E.flags[r] & 1u)) continue;
+          float* zb = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
+          zb[ty - 1] = 1.0f;
+          zb[3] = f32_quot(C->zone_cx[z] - E.px[r], fw, rw);
+          zb[4] = f32_quot(C->zone_cy[z] - E.py[r], fh, rh);
+          zb[5] = __double2float_rn(C->zone_ax[z]);
+          zb[6] = __double2float_rn(C->zone_ay[z]);
+          zb[7] = __double2float_rn(C->zone_effect[z]);
+        }
       }
       fence_proxy_async();
-      team_sync<W, TS>();
-      flush_stage<TS>(obs, gs, nr * D, stage, t);
+      __syncwarp();
+      flush_stage(obs, gs, nr * D, st, lane);
+      buf ^= 1;
     }
   }
   if (glob) {
     const int64_t gs = b * (int64_t)G;
-    float* row = gstage + (int)(gs & 3);
-    const float* own = &E.own[0][0];
-    for (int e = t; e < N * TABX_OWN_DIM; e += TS) {
+    float* st = stage + buf * SF;
+    float* row = st + (int)(gs & 3);
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    for (int e = lane; e < N * TABX_OWN_DIM; e += 32) {
       const int u = e / TABX_OWN_DIM;
       row[e] = E.own[u][e - u * TABX_OWN_DIM];
     }
-    (void)own;
-    for (int q = t; q < Z * TABX_ZONE_DIM; q += TS) {
+    for (int q = lane; q < Z * TABX_ZONE_DIM; q += 32) {
       const int z = q >> 3, f = q & 7;
       const int ty = C->zone_type[z];
       float v;
@@ -293,10 +271,11 @@ __device__ void emit_env(EmitEnv<W>& E, float* __restrict__ obs, float* __restri
       row[N * TABX_OWN_DIM + q] = v;
     }
     fence_proxy_async();
-    team_sync<W, TS>();
-    flush_stage<TS>(glob, gs, G, gstage, t);
+    __syncwarp();
+    flush_stage(glob, gs, G, st, lane);
   }
-  team_sync<W, TS>();
+  if (lane == 0) bulk_wait_read<0>();
+  __syncwarp();
 }
 
 // Stage geometry: R rows per chunk within `budget` bytes per buffer.
@@ -307,40 +286,27 @@ __host__ __device__ __forceinline__ int emit_rows(int N, int D, int budget) {
   return R;
 }
 __host__ __device__ __forceinline__ int emit_stage_floats(int N, int D, int G, int R) {
-  return (R * D + 8 + 3) & ~3;
-}
-__host__ __device__ __forceinline__ int emit_gstage_floats(int G) { return (G + 8 + 3) & ~3; }
-
-// Shared memory of one emitting team: view + stage + global-row stage.
-template <int W>
-__host__ __device__ __forceinline__ size_t emit_team_bytes(int N, int D, int G, int R) {
-  return ((sizeof(EmitEnv<W>) + 15) & ~(size_t)15) +
-         (size_t)(emit_stage_floats(N, D, G, R) + emit_gstage_floats(G)) * sizeof(float);
+  const int need = (R * D > G ? R * D : G) + 8;
+  return (need + 3) & ~3;
 }
 
 // K2: observations of every lane after a step (final_* buffers for lanes
 // whose auto-reset is pending: their terminal observation) or after
-// init_output.  One environment per CTA of EMIT_TS threads at a time
-// (persistent grid-stride); several CTAs per SM overlap their fills with
-// each other's TMA stores.
-constexpr int EMIT_TS = 128;
-constexpr int RESET_EMIT_BUDGET = 4096;  // stage bytes per env in the reset kernel
-constexpr int EMIT_BUDGET = 32768;  // stage bytes per CTA (whole env block up to 32 KB)
-
+// init_output.  EPW environments per CTA, one warp each; dynamic shared
+// memory = EPW x (view + 2 stage buffers of SF floats).
 #ifndef TABX_EMIT_MIN_BLOCKS
-#define TABX_EMIT_MIN_BLOCKS 5
+#define TABX_EMIT_MIN_BLOCKS 3
 #endif
-template <int W>
-__global__ void __launch_bounds__(EMIT_TS, TABX_EMIT_MIN_BLOCKS)
-    emit_kernel(const Params P, int R) {
+template <int W, int EPW>
+__global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS)
+    emit_kernel(const Params P, int R, int SF) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  EmitEnv<W>& E = *reinterpret_cast<EmitEnv<W>*>(smem_raw);
-  float* stage = reinterpret_cast<float*>(smem_raw + ((sizeof(EmitEnv<W>) + 15) & ~15));
-  float* gstage = stage + emit_stage_floats(P.N, P.D, P.G, R);
+  EmitEnv<W>* views = reinterpret_cast<EmitEnv<W>*>(smem_raw);
+  float* stages = reinterpret_cast<float*>(smem_raw + ((sizeof(EmitEnv<W>) * EPW + 15) & ~15));
   if (P.mode == MODE_STEP && P.sync->err_index != NO_ERROR) return;
-  const int t = threadIdx.x;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const DevState& st = P.st;
-  for (int64_t b = blockIdx.x; b < P.B; b += gridDim.x) {
+  for (int64_t b = (int64_t)blockIdx.x * EPW + w; b < P.B; b += (int64_t)gridDim.x * EPW) {
     const int32_t k = st.cfg[b];
     const tabx_config* C = P.cfgs + k;
     const DerivedCfg* DC = P.dcfgs + k;
@@ -348,31 +314,36 @@ __global__ void __launch_bounds__(EMIT_TS, TABX_EMIT_MIN_BLOCKS)
     float* ob = pending ? P.out.final_observations : P.out.observations;
     float* gb = pending ? P.out.final_global_state : P.out.global_state;
     if (!ob && !gb) continue;
-    load_view<W, EMIT_TS>(E, st, b, P.N, C, DC, t);
-    emit_env<W, EMIT_TS>(E, ob, gb, b, P.N, P.Z, P.D, P.G, R, stage, gstage, C, DC, t);
+    load_view<W>(views[w], st, b, P.N, C, DC, lane);
+    emit_lane<W>(views[w], ob, gb, b, P.N, P.Z, P.D, P.G, R, SF, stages + (size_t)w * 2 * SF, C,
+                 DC, lane);
   }
-  if (t == 0) bulk_wait_all();
+  if (lane == 0) bulk_wait_all();
 }
 
-template <int W>
+template <int W, int EPW>
 cudaError_t launch_emit_t(const Params& P, int sm_count, cudaStream_t stream) {
-  const int R = emit_rows(P.N, P.D, EMIT_BUDGET);
-  const size_t smem = emit_team_bytes<W>(P.N, P.D, P.G, R);
+  const int R = emit_rows(P.N, P.D, W == 1 ? 3200 : 8192);
+  const int SF = emit_stage_floats(P.N, P.D, P.G, R);
+  const size_t smem = ((sizeof(EmitEnv<W>) * EPW + 15) & ~(size_t)15) +
+                      (size_t)EPW * 2 * SF * sizeof(float);
   static size_t cached_smem = 0;
   static int per_sm = 0;
   if (smem != cached_smem) {
-    cudaError_t e = cudaFuncSetAttribute(emit_kernel<W>,
+    cudaError_t e = cudaFuncSetAttribute(emit_kernel<W, EPW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_kernel<W>, EMIT_TS, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_kernel<W, EPW>, 32 * EPW,
+                                                      smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
     cached_smem = smem;
   }
+  int64_t need = (P.B + EPW - 1) / EPW;
   int64_t cap = (int64_t)sm_count * per_sm;
-  int grid = (int)(P.B < cap ? P.B : cap);
+  int grid = (int)(need < cap ? need : cap);
   if (grid < 1) grid = 1;
-  emit_kernel<W><<<grid, EMIT_TS, smem, stream>>>(P, R);
+  emit_kernel<W, EPW><<<grid, 32 * EPW, smem, stream>>>(P, R, SF);
   return cudaGetLastError();
 }
 

@@ -718,14 +718,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     }
     env_sync<W>();
     if (emit && i < 32) {
-      const int R = emit_rows(N, P.D, RESET_EMIT_BUDGET);
-      float* stage = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(emit) +
-                                              ((sizeof(EmitEnv<W>) + 15) & ~(size_t)15));
-      float* gstage = stage + emit_stage_floats(N, P.D, P.G, R);
-      load_view<W, 32>(*emit, st, b, N, C, DC, i);
-      emit_env<W, 32>(*emit, O.observations, O.global_state, b, N, Z, P.D, P.G, R, stage, gstage,
-                      C, DC, i);
-      if (i == 0) bulk_wait_all();
+      const int R = emit_rows(N, P.D, W == 1 ? 3200 : 8192);
+      const int SF = emit_stage_floats(N, P.D, P.G, R);
+      float* stage = reinterpret_cast<float*>(emit + 1);
+      load_view<W>(*emit, st, b, N, C, DC, i);
+      emit_lane<W>(*emit, O.observations, O.global_state, b, N, Z, P.D, P.G, R, SF, stage, C, DC,
+                   i);
     }
     env_sync<W>();
     return;
@@ -1119,11 +1117,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   env_sync<W>();
 }
 
-// Per-env shared memory of the reset kernel's emitter (one warp per env).
+// Per-env shared memory of the reset kernel's emitter: view + 2 stage buffers.
 template <int W>
 __host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
-  const int R = emit_rows(P.N, P.D, RESET_EMIT_BUDGET);
-  return (emit_team_bytes<W>(P.N, P.D, P.G, R) + 15) & ~(size_t)15;
+  const int R = emit_rows(P.N, P.D, W == 1 ? 3200 : 8192);
+  const int SF = emit_stage_floats(P.N, P.D, P.G, R);
+  return ((sizeof(EmitEnv<W>) + 15) & ~(size_t)15) + (size_t)2 * SF * sizeof(float);
 }
 
 #ifndef TABX_MIN_BLOCKS

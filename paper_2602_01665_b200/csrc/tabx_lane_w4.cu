@@ -6,6 +6,6 @@ cudaError_t launch_lanes_w4(const Params& P, int sm_count, cudaStream_t stream, 
   return launch_lanes_t<4, 1>(P, sm_count, stream, grid);
 }
 cudaError_t launch_emit_w4(const Params& P, int sm_count, cudaStream_t stream) {
-  return launch_emit_t<4>(P, sm_count, stream);
+  return launch_emit_t<4, 2>(P, sm_count, stream);
 }
 }  // namespace tabx
