@@ -251,6 +251,7 @@ def run_gpu_arm(args) -> int:
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    sim.set_profiling(True)  # CUDA events around the step's three kernels
     with ClockSampler(local) as clk:
         t0.record(stream)
         for k in range(args.steps):
@@ -259,6 +260,8 @@ def run_gpu_arm(args) -> int:
             ends[k].record(stream)
         t1.record(stream)
         barrier()
+    kprof = sim.kernel_profile()
+    sim.set_profiling(False)
     elapsed_ms = max_over_ranks(t0.elapsed_time(t1))
     kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     value = total * args.steps / (elapsed_ms / 1000.0)
@@ -348,6 +351,22 @@ def run_gpu_arm(args) -> int:
         bytes_per = algorithmic_bytes(N, Z)
         kern_avg = statistics.mean(kern_ms)
         achieved = bytes_per * per / (kern_avg / 1000.0) / 1e9
+        D, G = sim_dims(N, Z)
+        obs_bytes = 4 * N * D + 4 * G + 57 * N + 5  # writes + the per-unit view it reads
+        step_bytes = bytes_per - (4 * N * D + 4 * G)
+        kernels = []
+        for name, ms, nbytes in (("step_kernel (K1: actions..rewards, caches, state)",
+                                  kprof["step_kernel_ms"], step_bytes),
+                                 ("obs_kernel (K2: observation + global-state stream, TMA)",
+                                  kprof["obs_kernel_ms"], obs_bytes),
+                                 ("reset_kernel (K3: deferred auto-resets)",
+                                  kprof["reset_kernel_ms"], None)):
+            ent = {"kernel": name, "ms_avg": ms}
+            if nbytes and ms > 0:
+                gbs = nbytes * per / (ms / 1000.0) / 1e9
+                ent.update({"bytes_per_env_step": nbytes, "achieved_gbs": gbs,
+                            "frac": gbs / peak})
+            kernels.append(ent)
         traffic = None
         prof = os.path.join(ROOT, "profiles", f"traffic_{args.scenario}.json")
         if os.path.exists(prof):
@@ -370,11 +389,15 @@ def run_gpu_arm(args) -> int:
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_env_step": bytes_per, "kernel_ms_avg": kern_avg,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+                         "scope": "one step = step kernel + observation kernel + reset kernel "
+                                  "(SURVEY.md 8(d) bytes per env-step x envs / step time)",
+                         "kernels": kernels,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks
+                         else "fallback"},
             "e2e": {"value": e2e_value, "unit": "env-steps/s",
                     "h2d_bytes_per_step": per * N * 8,
                     "d2h_bytes_per_step": per * N * 4 + 2 * per},
-            "gpu_launches": args.steps,
+            "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
             "episode_stats": stats,
         }

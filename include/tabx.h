@@ -244,6 +244,15 @@ int tabx_get_error(tabx_handle* h, tabx_error* err, int32_t clear);
  */
 int tabx_episode_stats(tabx_handle* h, double* dst_host, double* dst_device, int32_t reset);
 
+/*
+ * Per-kernel timing of tabx_step (CUDA events on the handle's stream around
+ * the step kernel, the observation kernel and the reset kernel).  With
+ * enable != 0 accumulation restarts; tabx_get_profile synchronises and
+ * returns the summed milliseconds ms[3] and the number of steps timed.
+ */
+int tabx_set_profiling(tabx_handle* h, int32_t enable);
+int tabx_get_profile(tabx_handle* h, double* ms, int64_t* steps);
+
 /* sizeof of the ABI structs, so bindings can check their mirrors. */
 int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state);
 

@@ -104,6 +104,8 @@ def lib() -> ct.CDLL:
         "tabx_get_error": (_i32, [P, ct.POINTER(TabxError), _i32]),
         "tabx_episode_stats": (_i32, [P, P, P, _i32]),
         "tabx_struct_sizes": (_i32, [P, P, P]),
+        "tabx_set_profiling": (_i32, [P, _i32]),
+        "tabx_get_profile": (_i32, [P, P, P]),
         "tabx_debug_sincos": (_i32, [P, P, P, _i64, P]),
     }
     for name, (res, args) in sig.items():

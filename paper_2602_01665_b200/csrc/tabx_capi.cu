@@ -49,7 +49,24 @@ struct tabx_handle {
   Sync* sync = nullptr;
   double* stats_dev = nullptr;
   const int64_t* last_actions = nullptr;
+  // optional per-kernel timing of tabx_step (bench roofline): ring of event sets
+  static constexpr int PROF_SLOTS = 256;
+  bool profiling = false;
+  cudaEvent_t prof_ev[PROF_SLOTS][4] = {};
+  int prof_next = 0, prof_pending = 0;
+  double prof_ms[3] = {0.0, 0.0, 0.0};
+  int64_t prof_steps = 0;
 };
+
+static void prof_collect(tabx_handle* h, int slot) {
+  float ms[3];
+  cudaEventSynchronize(h->prof_ev[slot][3]);
+  for (int k = 0; k < 3; ++k) {
+    cudaEventElapsedTime(&ms[k], h->prof_ev[slot][k], h->prof_ev[slot][k + 1]);
+    h->prof_ms[k] += ms[k];
+  }
+  h->prof_steps += 1;
+}
 
 static thread_local std::string g_err;
 
@@ -283,6 +300,9 @@ int tabx_destroy(tabx_handle* h) {
   if (!h) return TABX_OK;
   DeviceGuard guard(h->device);
   cudaStreamSynchronize(h->stream);
+  if (h->prof_ev[0][0])
+    for (int s = 0; s < tabx_handle::PROF_SLOTS; ++s)
+      for (int k = 0; k < 4; ++k) cudaEventDestroy(h->prof_ev[s][k]);
   cudaFree(h->dcfg_dev);
   cudaFree(h->cfg_dev);
   cudaFree(h->arena);
@@ -334,10 +354,25 @@ int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
   h->last_actions = actions;
   // K1 step logic -> K2 observation streaming -> K3 deferred auto-resets
   Params P = make_params(h, MODE_STEP, actions, out);
+  cudaEvent_t* ev = nullptr;
+  if (h->profiling) {
+    const int slot = h->prof_next;
+    if (h->prof_pending == tabx_handle::PROF_SLOTS) {
+      prof_collect(h, slot);
+      --h->prof_pending;
+    }
+    ev = h->prof_ev[slot];
+    h->prof_next = (slot + 1) % tabx_handle::PROF_SLOTS;
+    ++h->prof_pending;
+    cudaEventRecord(ev[0], h->stream);
+  }
   TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "step launch");
+  if (ev) cudaEventRecord(ev[1], h->stream);
   TABX_CUDA(launch_emit(P, h->W, h->sm_count, h->stream), "emit launch");
+  if (ev) cudaEventRecord(ev[2], h->stream);
   P.mode = MODE_RESET;
   TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "reset launch");
+  if (ev) cudaEventRecord(ev[3], h->stream);
   return TABX_OK;
 }
 
@@ -448,6 +483,32 @@ int tabx_episode_stats(tabx_handle* h, double* dst_host, double* dst_device, int
               "stats read");
     TABX_CUDA(cudaStreamSynchronize(h->stream), "stats sync");
   }
+  return TABX_OK;
+}
+
+int tabx_set_profiling(tabx_handle* h, int32_t enable) {
+  if (!h) return fail(TABX_E_ARGUMENT, "null handle");
+  DeviceGuard guard(h->device);
+  if (enable && !h->prof_ev[0][0]) {
+    for (int s = 0; s < tabx_handle::PROF_SLOTS; ++s)
+      for (int k = 0; k < 4; ++k) TABX_CUDA(cudaEventCreate(&h->prof_ev[s][k]), "event create");
+  }
+  h->profiling = enable != 0;
+  h->prof_next = h->prof_pending = 0;
+  h->prof_ms[0] = h->prof_ms[1] = h->prof_ms[2] = 0.0;
+  h->prof_steps = 0;
+  return TABX_OK;
+}
+
+int tabx_get_profile(tabx_handle* h, double* ms, int64_t* steps) {
+  if (!h || !ms) return fail(TABX_E_ARGUMENT, "tabx_get_profile: bad argument");
+  DeviceGuard guard(h->device);
+  const int first = (h->prof_next - h->prof_pending + tabx_handle::PROF_SLOTS) %
+                    tabx_handle::PROF_SLOTS;
+  for (int q = 0; q < h->prof_pending; ++q) prof_collect(h, (first + q) % tabx_handle::PROF_SLOTS);
+  h->prof_pending = 0;
+  for (int k = 0; k < 3; ++k) ms[k] = h->prof_ms[k];
+  if (steps) *steps = h->prof_steps;
   return TABX_OK;
 }
 

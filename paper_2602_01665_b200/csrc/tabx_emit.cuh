@@ -167,7 +167,15 @@ __device__ void emit_lane(const EmitEnv<W>& E, float* __restrict__ obs, float* _
       {
         const int n4 = (pad + nr * D + 3) >> 2;
         float4* z4 = reinterpret_cast<float4*>(st);
-        for (int q = lane; q < n4; q += 32) z4[q] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        const float4 zero = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        int q = lane;
+        for (; q + 96 < n4; q += 128) {
+          z4[q] = zero;
+          z4[q + 32] = zero;
+          z4[q + 64] = zero;
+          z4[q + 96] = zero;
+        }
+        for (; q < n4; q += 32) z4[q] = zero;
       }
       __syncwarp();
       for (int e = lane; e < nr * TABX_OWN_DIM; e += 32) {
@@ -294,6 +302,9 @@ __host__ __device__ __forceinline__ int emit_stage_floats(int N, int D, int G, i
 // whose auto-reset is pending: their terminal observation) or after
 // init_output.  EPW environments per CTA, one warp each; dynamic shared
 // memory = EPW x (view + 2 stage buffers of SF floats).
+#ifndef TABX_EMIT_BUDGET
+#define TABX_EMIT_BUDGET 3200  // stage bytes per buffer per warp (W = 1)
+#endif
 #ifndef TABX_EMIT_MIN_BLOCKS
 #define TABX_EMIT_MIN_BLOCKS 3
 #endif
@@ -323,7 +334,7 @@ __global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS)
 
 template <int W, int EPW>
 cudaError_t launch_emit_t(const Params& P, int sm_count, cudaStream_t stream) {
-  const int R = emit_rows(P.N, P.D, W == 1 ? 3200 : 8192);
+  const int R = emit_rows(P.N, P.D, W == 1 ? TABX_EMIT_BUDGET : 8192);
   const int SF = emit_stage_floats(P.N, P.D, P.G, R);
   const size_t smem = ((sizeof(EmitEnv<W>) * EPW + 15) & ~(size_t)15) +
                       (size_t)EPW * 2 * SF * sizeof(float);

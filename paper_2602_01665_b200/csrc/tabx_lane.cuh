@@ -718,7 +718,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     }
     env_sync<W>();
     if (emit && i < 32) {
-      const int R = emit_rows(N, P.D, W == 1 ? 3200 : 8192);
+      const int R = emit_rows(N, P.D, W == 1 ? TABX_EMIT_BUDGET : 8192);
       const int SF = emit_stage_floats(N, P.D, P.G, R);
       float* stage = reinterpret_cast<float*>(emit + 1);
       load_view<W>(*emit, st, b, N, C, DC, i);
@@ -1120,7 +1120,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 // Per-env shared memory of the reset kernel's emitter: view + 2 stage buffers.
 template <int W>
 __host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
-  const int R = emit_rows(P.N, P.D, W == 1 ? 3200 : 8192);
+  const int R = emit_rows(P.N, P.D, W == 1 ? TABX_EMIT_BUDGET : 8192);
   const int SF = emit_stage_floats(P.N, P.D, P.G, R);
   return ((sizeof(EmitEnv<W>) + 15) & ~(size_t)15) + (size_t)2 * SF * sizeof(float);
 }

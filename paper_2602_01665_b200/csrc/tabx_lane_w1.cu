@@ -6,6 +6,9 @@ cudaError_t launch_lanes_w1(const Params& P, int sm_count, cudaStream_t stream, 
   return launch_lanes_t<1, 4>(P, sm_count, stream, grid);
 }
 cudaError_t launch_emit_w1(const Params& P, int sm_count, cudaStream_t stream) {
-  return launch_emit_t<1, 8>(P, sm_count, stream);
+  #ifndef TABX_EMIT_EPW
+#define TABX_EMIT_EPW 8
+#endif
+  return launch_emit_t<1, TABX_EMIT_EPW>(P, sm_count, stream);
 }
 }  // namespace tabx

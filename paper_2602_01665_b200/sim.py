@@ -310,6 +310,20 @@ class BatchSim:
                 "sum_return", "eliminations", "env_steps")
         return dict(zip(keys, list(host)))
 
+    def set_profiling(self, enable: bool = True) -> None:
+        """Time the step's three kernels with CUDA events (restarts the sums)."""
+        nat.check(nat.lib().tabx_set_profiling(self._h, int(enable)), "tabx_set_profiling")
+
+    def kernel_profile(self) -> dict:
+        """Average milliseconds per step of each kernel since set_profiling (syncs)."""
+        ms = (ct.c_double * 3)()
+        n = ct.c_int64()
+        with torch.cuda.device(self.device):
+            nat.check(nat.lib().tabx_get_profile(self._h, ms, ct.byref(n)), "tabx_get_profile")
+        k = max(n.value, 1)
+        return {"steps": n.value, "step_kernel_ms": ms[0] / k, "obs_kernel_ms": ms[1] / k,
+                "reset_kernel_ms": ms[2] / k}
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             nat.lib().tabx_destroy(self._h)
