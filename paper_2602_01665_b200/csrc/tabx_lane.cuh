@@ -63,6 +63,10 @@ struct EnvSmem {
   uint32_t m_zone[TABX_MAX_ZONES][W];
   double red[2];
   double part[16];
+  // W == 1: unordered pairs (i<j) in row-major order, (i << 8) | j, and the
+  // touching-pair bit masks of one step (32 pairs per word, same order)
+  uint16_t ptab[W == 1 ? 496 : 1];
+  uint32_t tmask[W == 1 ? 16 : 1];
 };
 
 template <int W>
@@ -145,11 +149,12 @@ __device__ __forceinline__ bool bit_of(const uint32_t* row, int j) {
 // within 3 ulp of fl64(x / y), so both round to the same float32 unless q
 // sits within a few ulp of a float32 rounding midpoint (low 29 mantissa bits
 // near 0x10000000) -- then, and for float32-subnormal magnitudes, divide.
+// Only the swamps the unit stands in contribute (the reference multiplies the
+// others' 1.0, which is exact), in ascending zone order.
 __device__ __forceinline__ double swamp_mult(const tabx_config* __restrict__ C, int Z,
                                              uint32_t zin, uint32_t swamp_m) {
   double m = 1.0;
-  uint32_t hit = zin & swamp_m;
-  for (int z = 0; z < Z; ++z) m = m * (((hit >> z) & 1u) ? C->zone_effect[z] : 1.0);
+  for (uint32_t hit = zin & swamp_m; hit; hit &= hit - 1) m = m * C->zone_effect[__ffs(hit) - 1];
   return m;
 }
 
@@ -157,10 +162,9 @@ __device__ __forceinline__ double swamp_mult(const tabx_config* __restrict__ C, 
 __device__ __forceinline__ double lava_sum(const tabx_config* __restrict__ C, int Z, uint32_t zin,
                                            uint32_t lava_m) {
   uint32_t hit = zin & lava_m;
-  if (Z < 8) {
+  if (Z < 8) {  // sequential from 0.0; the 0.0 terms of other zones are exact no-ops
     double r = 0.0;
-    for (int z = 0; z < Z; ++z)
-      if ((hit >> z) & 1u) r += C->zone_effect[z];
+    for (; hit; hit &= hit - 1) r += C->zone_effect[__ffs(hit) - 1];
     return r;
   }
   double v[TABX_MAX_ZONES];
@@ -170,12 +174,18 @@ __device__ __forceinline__ double lava_sum(const tabx_config* __restrict__ C, in
 
 // Index of the floor(u*n)-th legal action (environment.py:198-201).
 __device__ __forceinline__ int kth_legal(uint32_t mask7, double u) {
-  int n = __popc(mask7);
-  long long k = (long long)(u * (double)n);
-  if (k > n - 1) k = n - 1;
-  uint32_t m = mask7;
-  for (long long s = 0; s < k; ++s) m &= m - 1;
-  return __ffs(m) - 1;
+  const int n = __popc(mask7);
+  long long kk = (long long)(u * (double)n);
+  if (kk > n - 1) kk = n - 1;
+  // position of the kk-th set bit of the 7-bit mask, by popc halving
+  int k = (int)kk, pos = 0;
+  uint32_t w = mask7;
+  int c = __popc(w & 0xFu);
+  if (k >= c) { k -= c; w >>= 4; pos += 4; }
+  c = __popc(w & 0x3u);
+  if (k >= c) { k -= c; w >>= 2; pos += 2; }
+  if (k >= (int)(w & 1u)) pos += 1;
+  return pos;
 }
 
 // Move choice: argmin / argmax of squared distance over the 4 axis moves
@@ -465,7 +475,8 @@ template <int W>
 __device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
                                int N, int Z, const UnitStatic& U, const uint32_t (&vis)[W],
                                const uint32_t (&atk)[W], double hd, double cd, double step,
-                               uint32_t mask7, double u_explore, double u_pick, double eps,
+                               uint32_t mask7, double u_explore, uint64_t seed, uint64_t t_step,
+                               double eps,
                                double xi, uint32_t bush_m, double& mx, double& my, bool& memv) {
   const double px = S.px[i], py = S.py[i];
   // target candidates: visible, alive & active, not self
@@ -558,7 +569,8 @@ __device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_conf
     act = best_move(px, py, C->zone_cx[nb], C->zone_cy[nb], step, false);
   }
   if (act < 0) act = A_ROTATE;
-  if (u_explore < eps) act = kth_legal(mask7, u_pick);
+  // epsilon exploration; the pick draw is only needed when exploring
+  if (u_explore < eps) act = kth_legal(mask7, uniform53(seed, t_step, TAG_PICK, (uint64_t)i));
   if (has) {
     mx = tpx;
     my = tpy;
@@ -801,6 +813,8 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const bool ctl = alive && U.active;
   const uint32_t mask7 = ctl ? (0x1Fu | ((cd <= 0.0) ? 0x20u : 0u) | (C->enable_noop ? 0x40u : 0u))
                              : 0x40u;
+  // effective speed after swamps at the pre-move position (arrays.py:338-343)
+  const double speff = U.speed * swamp_mult(C, Z, S.zin[i], swamp_m);
   // 2. action resolution (environment.py:154-204)
   const int team = U.enemy ? 1 : 0;
   const int ctrl = C->controller[team];
@@ -829,10 +843,10 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     }
     if (heur) {
       const double ue = uniform53(seed, (uint64_t)(int64_t)t, TAG_EXPLORE, (uint64_t)i);
-      const double up = uniform53(seed, (uint64_t)(int64_t)t, TAG_PICK, (uint64_t)i);
-      const double stepl = (U.speed * swamp_mult(C, Z, S.zin[i], swamp_m)) * dt;
-      act = scripted_action<W>(S, C, i, N, Z, U, vis, atk, hd, cd, stepl, mask7, ue, up,
-                               C->epsilon[team], C->aggressive[team], bush_m, mx, my, memv);
+      const double stepl = speff * dt;
+      act = scripted_action<W>(S, C, i, N, Z, U, vis, atk, hd, cd, stepl, mask7, ue, seed,
+                               (uint64_t)(int64_t)t, C->epsilon[team], C->aggressive[team],
+                               bush_m, mx, my, memv);
     }
   }
   if (free_u && ctrl == TABX_CTRL_RANDOM)
@@ -841,7 +855,6 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 
   // 3-4. commanded velocity, integration, timers (environment.py:215-228)
   const bool moving = act < 4 && alive && U.active && !U.kin;
-  const double speff = U.speed * swamp_mult(C, Z, S.zin[i], swamp_m);
   const double vmag = moving ? speff : 0.0;
   const int ad = act < 0 ? 0 : (act > 3 ? 3 : act);
   const double dirx = ad == 2 ? 1.0 : (ad == 3 ? -1.0 : 0.0);
@@ -861,45 +874,79 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   env_sync<W>();
 
   // 5. contacts: detection (physics.py:27-49), Gauss-Seidel (physics.py:52-94)
-  uint32_t trow[W];
-#pragma unroll
-  for (int k = 0; k < W; ++k) trow[k] = 0u;
+  // float32 filter on squared distance vs rs^2 (margin 1e-5 relative);
+  // near-contact pairs get the reference's float64 depth test
   bool any_touch = false;
-  if (valid && U.active && running) {
-    // float32 filter on squared distance vs rs^2 (margin 1e-5 relative);
-    // near-contact pairs get the reference's float64 depth test
-    uint32_t unsure[W];
-#pragma unroll
-    for (int k = 0; k < W; ++k) unsure[k] = 0u;
-    for (int j = i + 1; j < N; ++j) {
-      const float dxf = (float)(S.px[j] - px), dyf = (float)(S.py[j] - py);
-      const float d2f = dxf * dxf + dyf * dyf;
-      const float rs2f = (float)((U.rad + S.rad[j]) * (U.rad + S.rad[j]));
-      const bool sure = (d2f < rs2f * 0.99999f) & (d2f > 1e-30f);
-      const bool maybe = !sure & !(d2f > rs2f * 1.00001f);
-      trow[j >> 5] |= (uint32_t)sure << (j & 31);
-      unsure[j >> 5] |= (uint32_t)maybe << (j & 31);
-    }
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-      trow[k] &= S.m_active[k];
-      uint32_t m = unsure[k] & S.m_active[k];
-      while (m) {
-        const int j = (k << 5) + __ffs(m) - 1;
-        m &= m - 1;
-        const double dx = S.px[j] - px, dy = S.py[j] - py;
-        const double rs = U.rad + S.rad[j];
-        const double dist = slow_sqrt(dx * dx + dy * dy);
-        const double depth = dist == 0.0 ? rs : rs - dist;
-        if (depth > 0.0) trow[k] |= 1u << (j & 31);
+  if (W == 1) {
+    // all 32 lanes over the N(N-1)/2 pairs; one ballot word per 32 pairs keeps
+    // the ascending (i, j) order the Gauss-Seidel solve needs
+    const int NP = N * (N - 1) / 2;
+    uint32_t anyw = 0u;
+    for (int k = 0; (k << 5) < NP; ++k) {
+      const int p = (k << 5) + i;
+      bool hit = false;
+      if (p < NP && running) {
+        const uint32_t ij = S.ptab[p];
+        const int a = (int)(ij >> 8), c = (int)(ij & 255u);
+        if (S.uf[a] & S.uf[c] & UF_ACTIVE) {
+          const double dx = S.px[c] - S.px[a], dy = S.py[c] - S.py[a];
+          const double rs = S.rad[a] + S.rad[c];
+          const float dxf = (float)dx, dyf = (float)dy;
+          const float d2f = dxf * dxf + dyf * dyf;
+          const float rs2f = (float)(rs * rs);
+          if (d2f < rs2f * 0.99999f && d2f > 1e-30f) {
+            hit = true;
+          } else if (!(d2f > rs2f * 1.00001f)) {
+            const double dist = slow_sqrt(dx * dx + dy * dy);
+            hit = (dist == 0.0 ? rs : rs - dist) > 0.0;
+          }
+        }
       }
-      any_touch |= trow[k] != 0u;
+      const uint32_t bm = __ballot_sync(0xffffffffu, hit);
+      if (i == 0) S.tmask[k] = bm;
+      anyw |= bm;
     }
-  }
-  double vfx = vux, vfy = vuy;
-  if (env_any<W>(any_touch, S, i)) {
+    any_touch = anyw != 0u;
+  } else {
+    uint32_t trow[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) trow[k] = 0u;
+    bool mine = false;
+    if (valid && U.active && running) {
+      uint32_t unsure[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) unsure[k] = 0u;
+      for (int j = i + 1; j < N; ++j) {
+        const float dxf = (float)(S.px[j] - px), dyf = (float)(S.py[j] - py);
+        const float d2f = dxf * dxf + dyf * dyf;
+        const float rs2f = (float)((U.rad + S.rad[j]) * (U.rad + S.rad[j]));
+        const bool sure = (d2f < rs2f * 0.99999f) & (d2f > 1e-30f);
+        const bool maybe = !sure & !(d2f > rs2f * 1.00001f);
+        trow[j >> 5] |= (uint32_t)sure << (j & 31);
+        unsure[j >> 5] |= (uint32_t)maybe << (j & 31);
+      }
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        trow[k] &= S.m_active[k];
+        uint32_t m = unsure[k] & S.m_active[k];
+        while (m) {
+          const int j = (k << 5) + __ffs(m) - 1;
+          m &= m - 1;
+          const double dx = S.px[j] - px, dy = S.py[j] - py;
+          const double rs = U.rad + S.rad[j];
+          const double dist = slow_sqrt(dx * dx + dy * dy);
+          const double depth = dist == 0.0 ? rs : rs - dist;
+          if (depth > 0.0) trow[k] |= 1u << (j & 31);
+        }
+        mine |= trow[k] != 0u;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < W; ++k) S.touch[i * W + k] = trow[k];
+    any_touch = env_any<W>(mine, S, i);
+  }
+  double vfx = vux, vfy = vuy;
+  if (any_touch) {
     S.vx[i] = vux;
     S.vy[i] = vuy;
     S.sx[i] = 0.0;
@@ -907,12 +954,19 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     env_sync<W>();
     if (i == 0) {
       const double e = C->restitution, slop = C->slop, beta = C->correction;
-      for (int a = 0; a < N; ++a) {
-        for (int k = 0; k < W; ++k) {
-          uint32_t m = S.touch[a * W + k];
+      const int NP = N * (N - 1) / 2;
+      for (int a0 = 0; a0 < (W == 1 ? 1 : N); ++a0) {
+        for (int k = 0; k < (W == 1 ? (NP + 31) >> 5 : W); ++k) {
+          uint32_t m = W == 1 ? S.tmask[k] : S.touch[a0 * W + k];
           while (m) {
-            const int bb = (k << 5) + __ffs(m) - 1;
+            int a = a0;
+            int bb = (k << 5) + __ffs(m) - 1;
             m &= m - 1;
+            if (W == 1) {  // pair index -> (a, bb)
+              const uint32_t ij = S.ptab[bb];
+              a = (int)(ij >> 8);
+              bb = (int)(ij & 255u);
+            }
             const double wa = C->inv_mass[a], wb = C->inv_mass[bb];
             const double w = wa + wb;
             if (!(w > 0.0)) continue;
@@ -985,12 +1039,19 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const bool landed = running && swing && tgt >= 0;
   S.tgt[i] = landed ? tgt : -1;
   env_sync<W>();
+  // per-victim damage: landed attackers in ascending order (combat.py:108)
+  uint32_t lm[W];
+  env_ballot<W>(landed, S, i, lm);
   double delta = 0.0;
   bool was_hit = false;
-  for (int a = 0; a < N; ++a) {
-    if (S.tgt[a] == i) {
-      delta += S.dmg[a];
-      was_hit = true;
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    for (uint32_t m = lm[k]; m; m &= m - 1) {
+      const int a = (k << 5) + __ffs(m) - 1;
+      if (S.tgt[a] == i) {
+        delta += S.dmg[a];
+        was_hit = true;
+      }
     }
   }
   if (running) {
@@ -1152,6 +1213,15 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
   }
   const int g = threadIdx.x / (32 * W);
   const int i = threadIdx.x % (32 * W);
+  if (W == 1) {  // pair table of this env group (N <= 32)
+    int p = 0;
+    for (int a = 0; a < P.N; ++a) {
+      const int cnt = P.N - 1 - a;
+      for (int q = i; q < cnt; q += 32) envs[g].ptab[p + q] = (uint16_t)((a << 8) | (a + 1 + q));
+      p += cnt;
+    }
+    __syncwarp();
+  }
   for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB) {
     if (P.mode == MODE_RESET && !(P.st.flags[b] & F_PEND)) continue;  // env-uniform
     run_lane<W>(P, b, i, envs[g],
