@@ -266,8 +266,9 @@ __global__ void stats_kernel(DevState st, int64_t B, double* out, int reset) {
 __global__ void sincos_debug_kernel(const double* x, double* s, double* c, int64_t n) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
-    s[k] = libm_sin(x[k]);
-    c[k] = libm_cos(x[k]);
+    const sincos_t r = libm_sincos(x[k]);
+    s[k] = r.s;
+    c[k] = r.c;
   }
 }
 

@@ -526,7 +526,8 @@ __device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_conf
   if (act < 0 && has) {
     // _aligned_after_rotate (heuristics.py:87-100): heading + rot_step unwrapped
     const double h2 = hd + C->rot_step;
-    const double c2 = libm_cos(h2), s2 = libm_sin(h2);
+    const sincos_t sc2 = libm_sincos(h2);
+    const double c2 = sc2.c, s2 = sc2.s;
     const double dx = tpx - px, dy = tpy - py;
     const double lx = dx * c2 + dy * s2;
     const double ly = (-dx) * s2 + dy * c2;
@@ -619,12 +620,13 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     const double2 iv = st.imp_dv[u];
     ivx = iv.x;
     ivy = iv.y;
-    const double2 vv = st.vel[u];
-    vlx = vv.x;
-    vly = vv.y;
-    const double2 m = st.mem_pos[u];
-    mx = m.x;
-    my = m.y;
+    // realized velocity is output-only (written back only by running lanes);
+    // the scripted-controller memory only exists for heuristic-team units
+    if (P.mode == MODE_STEP && C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC) {
+      const double2 m = st.mem_pos[u];
+      mx = m.x;
+      my = m.y;
+    }
     const uint8_t ub = st.ubits[u];
     alive = ub & U_ALIVE;
     memv = ub & U_MEMV;
@@ -680,8 +682,11 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     winner = -1;
     reason = R_NONE;
     fk = -1;
-    ch = libm_cos(hd);
-    sh = libm_sin(hd);
+    {
+      const sincos_t sc = libm_sincos(hd);
+      ch = sc.c;
+      sh = sc.s;
+    }
     zin = valid ? zone_bits(C, DC, Z, px, py) : 0u;
     publish();
     build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
@@ -1017,8 +1022,11 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   // 7. rotation (environment.py:249-252)
   if (act == A_ROTATE && alive && U.active && running) {
     hd = np_remainder(hd + C->rot_step, 6.283185307179586);
-    ch = libm_cos(hd);
-    sh = libm_sin(hd);
+    {
+      const sincos_t sc = libm_sincos(hd);
+      ch = sc.c;
+      sh = sc.s;
+    }
   }
 
   // 8. caches at the post-move state (environment.py:254-257)
@@ -1151,12 +1159,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   if (valid) {
     st.pos[u] = make_double2(px, py);
     st.heading[u] = hd;
-    st.vel[u] = make_double2(vlx, vly);
+    if (running) st.vel[u] = make_double2(vlx, vly);
     st.imp_dv[u] = make_double2(ivx, ivy);
     st.health[u] = hp;
     st.cooldown[u] = cd;
     st.reveal[u] = rv;
-    st.mem_pos[u] = make_double2(mx, my);
+    if (C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC) st.mem_pos[u] = make_double2(mx, my);
     st.hcs[u] = make_double2(ch, sh);
     st.zbits[u] = zin;
     st.ubits[u] = (alive ? U_ALIVE : 0) | (memv ? U_MEMV : 0);

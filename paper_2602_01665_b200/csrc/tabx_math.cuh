@@ -163,6 +163,26 @@ TABX_HD_CALL double libm_cos(double x) {
   return cos(x);
 }
 
+// (sin x, cos x) with the large-argument reduction shared; each component is
+// exactly libm_sin(x) / libm_cos(x).
+struct sincos_t {
+  double s, c;
+};
+TABX_HD_CALL sincos_t libm_sincos(double x) {
+  sincos_t r;
+  const uint32_t k = (uint32_t)(d_to_bits(x) >> 32) & 0x7fffffffu;
+  if (k >= 0x400368fdu && k < 0x419921FBu) {
+    double a, da;
+    const int n = libm_reduce(x, &a, &da);
+    r.s = libm_do_sincos(a, da, n);
+    r.c = libm_do_sincos(a, da, n + 1);
+  } else {
+    r.s = libm_sin(x);
+    r.c = libm_cos(x);
+  }
+  return r;
+}
+
 // numpy.maximum / numpy.minimum for non-NaN operands (loops_minmax: in1 >= in2 ? in1 : in2)
 TABX_HD double np_max(double a, double b) { return a >= b ? a : b; }
 TABX_HD double np_min(double a, double b) { return a <= b ? a : b; }

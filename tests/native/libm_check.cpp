@@ -23,6 +23,12 @@ int main(int argc, char** argv) {
       fwrite(&s, 8, 1, g);
       fwrite(&c, 8, 1, g);
     }
+  } else if (!strcmp(argv[1], "sincos2")) {
+    for (double v : xs) {
+      const tabx::sincos_t r = tabx::libm_sincos(v);
+      fwrite(&r.s, 8, 1, g);
+      fwrite(&r.c, 8, 1, g);
+    }
   } else if (!strcmp(argv[1], "pairwise")) {
     int n = atoi(argv[4]);
     for (size_t r = 0; r + n <= xs.size(); r += n) {

@@ -59,10 +59,11 @@ def test_sin_cos_match_numpy(tool):
         np.array([0.0, -0.0, 5e-324, 2.0 ** -27, 2.0 ** -26, 0.126, 0.85546875, 2.426265,
                   np.pi, 2 * np.pi, np.radians(180.0), np.radians(30.0)]),
     ])
-    y = _run(tool, "sincos", x).reshape(-1, 2)
-    bad_s = np.nonzero(y[:, 0] != np.sin(x))[0]
-    bad_c = np.nonzero(y[:, 1] != np.cos(x))[0]
-    assert len(bad_s) == 0 and len(bad_c) == 0, (x[bad_s[:5]], x[bad_c[:5]])
+    for mode in ("sincos", "sincos2"):  # separate calls / shared reduction
+        y = _run(tool, mode, x).reshape(-1, 2)
+        bad_s = np.nonzero(y[:, 0] != np.sin(x))[0]
+        bad_c = np.nonzero(y[:, 1] != np.cos(x))[0]
+        assert len(bad_s) == 0 and len(bad_c) == 0, (mode, x[bad_s[:5]], x[bad_c[:5]])
 
 
 @pytest.mark.parametrize("n", [1, 3, 6, 7, 8, 9, 15, 16, 20, 31, 100, 127, 128, 129, 200, 256])
