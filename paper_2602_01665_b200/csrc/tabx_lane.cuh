@@ -470,14 +470,20 @@ __device__ __forceinline__ void team_ratios(EnvSmem<W>& S, int i, int N, bool ac
 }
 
 // Heuristic opponent decision for unit i (heuristics.py:103-243).
-// Returns the action and updates the scripted-controller memory.
+// Returns the action packed with the scripted-controller memory update.
+constexpr int SA_ACT_MASK = 0xff, SA_HAS = 0x100, SA_MEMOK = 0x200, SA_TGT_SHIFT = 16;
 template <int W>
 __device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
-                               int N, int Z, const UnitStatic& U, const uint32_t (&vis)[W],
-                               const uint32_t (&atk)[W], double hd, double cd, double step,
+                               int N, int Z, double hd, double cd, double step,
                                uint32_t mask7, double u_explore, uint64_t seed, uint64_t t_step,
-                               double eps,
-                               double xi, uint32_t bush_m, double& mx, double& my, bool& memv) {
+                               double eps, double xi, uint32_t bush_m, double mx, double my,
+                               bool memv) {
+  // everything arrives by value (scalars in registers, the unit's vis/atk rows
+  // in S.vis / S.atk): reference parameters of a non-inlined call would force
+  // the caller's copies into local memory
+  const UnitStatic U = load_static(C, i, true);
+  const uint32_t* vis = &S.vis[i * W];
+  const uint32_t* atk = &S.atk[i * W];
   const double px = S.px[i], py = S.py[i];
   // target candidates: visible, alive & active, not self
   // squared distances; closer() orders them exactly as their float64 roots
@@ -572,12 +578,8 @@ __device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_conf
   if (act < 0) act = A_ROTATE;
   // epsilon exploration; the pick draw is only needed when exploring
   if (u_explore < eps) act = kth_legal(mask7, uniform53(seed, t_step, TAG_PICK, (uint64_t)i));
-  if (has) {
-    mx = tpx;
-    my = tpy;
-  }
-  memv = has || mem_ok;
-  return act;
+  // packed result: action, memory update (has -> remember tgt; memv = has || mem_ok)
+  return act | (has ? SA_HAS : 0) | (mem_ok ? SA_MEMOK : 0) | (tgt << SA_TGT_SHIFT);
 }
 
 // ---------------------------------------------------------------- lane ---
@@ -847,11 +849,25 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
       for (int k = 0; k < W; ++k) vis[k] = atk[k] = 0u;
     }
     if (heur) {
+      if (!refresh) {  // the refreshed rows are already in S.vis / S.atk
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          S.vis[i * W + k] = vis[k];
+          S.atk[i * W + k] = atk[k];
+        }
+      }
       const double ue = uniform53(seed, (uint64_t)(int64_t)t, TAG_EXPLORE, (uint64_t)i);
       const double stepl = speff * dt;
-      act = scripted_action<W>(S, C, i, N, Z, U, vis, atk, hd, cd, stepl, mask7, ue, seed,
-                               (uint64_t)(int64_t)t, C->epsilon[team], C->aggressive[team],
-                               bush_m, mx, my, memv);
+      const int r = scripted_action<W>(S, C, i, N, Z, hd, cd, stepl, mask7, ue, seed,
+                                       (uint64_t)(int64_t)t, C->epsilon[team],
+                                       C->aggressive[team], bush_m, mx, my, memv);
+      act = r & SA_ACT_MASK;
+      if (r & SA_HAS) {
+        const int tg = r >> SA_TGT_SHIFT;
+        mx = S.px[tg];
+        my = S.py[tg];
+      }
+      memv = (r & (SA_HAS | SA_MEMOK)) != 0;
     }
   }
   if (free_u && ctrl == TABX_CTRL_RANDOM)
