@@ -211,6 +211,24 @@ __global__ void derive_kernel(const tabx_config* __restrict__ cfgs, DerivedCfg* 
       D->rax[z] = C->zone_type[z] ? 1.0 / C->zone_ax[z] : 0.0;
       D->ray[z] = C->zone_type[z] ? 1.0 / C->zone_ay[z] : 0.0;
     }
+    // zone blocks of the observation / global state (perception.py:170-201)
+    for (int q = threadIdx.x; q < TABX_MAX_ZONES * TABX_ZONE_DIM; q += blockDim.x) {
+      const int z = q / TABX_ZONE_DIM, f = q % TABX_ZONE_DIM;
+      const int ty = z < C->n_zones ? C->zone_type[z] : TABX_ZONE_NONE;
+      float vo = 0.0f, vg = 0.0f;
+      if (ty != TABX_ZONE_NONE) {
+        switch (f) {
+          case 0: case 1: case 2: vo = vg = (ty == f + 1) ? 1.0f : 0.0f; break;
+          case 3: vg = __double2float_rn(C->zone_cx[z] / C->field_w); break;
+          case 4: vg = __double2float_rn(C->zone_cy[z] / C->field_h); break;
+          case 5: vo = vg = __double2float_rn(C->zone_ax[z]); break;
+          case 6: vo = vg = __double2float_rn(C->zone_ay[z]); break;
+          default: vo = vg = __double2float_rn(C->zone_effect[z]); break;
+        }
+      }
+      D->zobs[q] = vo;
+      D->zglob[q] = vg;
+    }
     if (threadIdx.x == 0) {
       D->rw = 1.0 / C->field_w;
       D->rh = 1.0 / C->field_h;

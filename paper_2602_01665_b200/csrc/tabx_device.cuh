@@ -80,6 +80,11 @@ struct DerivedCfg {
   double rucd[TABX_MAX_UNITS];        // 1/cooldown (0 if cooldown == 0)
   uint32_t lava_m, bush_m, swamp_m;   // zone-type bit masks
   int32_t n_ally, n_enemy;            // team roster sizes (active units)
+  // float32 zone blocks (perception.py:170-201), zeros for unused slots:
+  // observation block with the two relative-position features left 0, and
+  // the global-state block (absolute position / field size)
+  float zobs[TABX_MAX_ZONES * TABX_ZONE_DIM];
+  float zglob[TABX_MAX_ZONES * TABX_ZONE_DIM];
 };
 
 enum Mode : int { MODE_STEP = 0, MODE_INIT = 1, MODE_REFRESH = 2, MODE_RESET = 3 };
@@ -138,9 +143,14 @@ static __device__ __noinline__ double slow_sqrt(double x) { return sqrt(x); }
 
 __device__ __forceinline__ float f32_quot(double x, double y, double ry) {
   double q = x * ry;
-  const int dlt = (int)((uint32_t)__double2loint(q) & 0x1FFFFFFFu) - 0x10000000;
-  const double aq = fabs(q);
-  if ((dlt <= 8 && dlt >= -8) || (aq < 2.4e-38 && aq != 0.0) || aq > 1e37) q = slow_div(x, y);
+  const uint32_t lo = (uint32_t)__double2loint(q), hi = (uint32_t)__double2hiint(q);
+  // low 29 bits within 8 of the float32 rounding midpoint 0x10000000
+  const bool mid = ((lo - 0x0FFFFFF8u) & 0x1FFFFFFFu) <= 16u;
+  // |q| outside [2^-125, 2^123) (float32 subnormal / overflow range, inf, nan)
+  // and not zero
+  const uint32_t e = (hi >> 20) & 0x7FFu;
+  const bool odd = (e - 898u) > 247u && ((hi & 0x7FFFFFFFu) | lo) != 0u;
+  if (mid || odd) q = slow_div(x, y);
   return __double2float_rn(q);
 }
 

@@ -17,15 +17,38 @@
 
 namespace tabx {
 
-// Per-warp view of one environment (units 0..32W-1).
+// Per-warp view of one environment, laid out in dynamic shared memory for
+// the batch's N units: positions, the 15 own features (16-float rows), the
+// N-bit visibility / attackable rows, unit flags.
 template <int W>
 struct EmitEnv {
-  static constexpr int NT = 32 * W;
-  double px[NT], py[NT];
-  float own[NT][16] __attribute__((aligned(16)));
-  uint32_t vis[NT * W], atk[NT * W];
-  uint32_t flags[NT];  // bit0 active, bit1 enemy
+  double* px;
+  double* py;
+  float (*own)[16];
+  uint32_t* vis;
+  uint32_t* atk;
+  uint32_t* flags;  // bit0 active, bit1 enemy
 };
+
+// Per-warp emitter scratch: the view and, for W == 1, the zone-relative
+// positions of every (observer, zone) and the visible-pair list of one chunk
+// of rows; then two stage buffers.
+template <int W>
+struct EmitScratch {
+  EmitEnv<W> E;
+  float2* zq;       // [N * Z]
+  uint16_t* clist;  // [R * 32], (row-in-chunk << 5) | j
+  float* stage;
+};
+__host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+template <int W>
+__host__ __device__ __forceinline__ size_t emit_view_bytes(int N) {
+  return align16((size_t)16 * N) + (size_t)64 * N + align16((size_t)4 * N * (2 * W + 1));
+}
+template <int W>
+__host__ __device__ __forceinline__ size_t emit_aux_bytes(int N, int Z, int R) {
+  return W == 1 ? align16((size_t)N * Z * sizeof(float2) + (size_t)R * 32 * sizeof(uint16_t)) : 0;
+}
 
 __device__ __forceinline__ bool row_bit(const uint32_t* row, int j) {
   return (row[j >> 5] >> (j & 31)) & 1u;
@@ -64,9 +87,10 @@ __device__ __forceinline__ void own_from_state(float* o, const DevState& st, int
 
 // Load lane b's view into E (all 32 lanes of the warp).
 template <int W>
-__device__ __forceinline__ void load_view(EmitEnv<W>& E, const DevState& st, int64_t b, int N,
-                                          const tabx_config* __restrict__ C,
+__device__ __forceinline__ void load_view(const EmitScratch<W>& X, const DevState& st, int64_t b,
+                                          int N, int Z, const tabx_config* __restrict__ C,
                                           const DerivedCfg* __restrict__ DC, int lane) {
+  const EmitEnv<W>& E = X.E;
   for (int u = lane; u < N; u += 32) {
     const int64_t gu = b * N + u;
     const double2 p = st.pos[gu];
@@ -78,6 +102,18 @@ __device__ __forceinline__ void load_view(EmitEnv<W>& E, const DevState& st, int
     for (int k = 0; k < W; ++k) {
       E.vis[u * W + k] = st.vis[gu * W + k];
       E.atk[u * W + k] = st.atk[gu * W + k];
+    }
+  }
+  if constexpr (W == 1) {
+    // zone-relative positions of each active observer (perception.py:184-185)
+    if (lane < N && (E.flags[lane] & 1u)) {
+      const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
+      const double px = E.px[lane], py = E.py[lane];
+      for (int z = 0; z < Z; ++z) {
+        if (C->zone_type[z] == TABX_ZONE_NONE) continue;
+        X.zq[lane * Z + z] = make_float2(f32_quot(C->zone_cx[z] - px, fw, rw),
+                                         f32_quot(C->zone_cy[z] - py, fh, rh));
+      }
     }
   }
   __syncwarp();
@@ -115,15 +151,17 @@ __device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs,
   const int64_t a0 = (gs + 3) & ~(int64_t)3;
   const int64_t a1 = (gs + count) & ~(int64_t)3;
   if (a1 > a0) {
-    if (lane == 0) {
-      bulk_s2g(dst + a0, stage + pad + (a0 - gs), (uint32_t)((a1 - a0) * 4));
-      bulk_commit();
-    }
-    for (int e = lane; e < (int)(a0 - gs); e += 32) dst[gs + e] = stage[pad + e];
-    for (int e = (int)(a1 - gs) + lane; e < count; e += 32) dst[gs + e] = stage[pad + e];
+    if (lane == 0) bulk_s2g(dst + a0, stage + pad + (a0 - gs), (uint32_t)((a1 - a0) * 4));
+    // <= 3 head floats on lanes 0..2, <= 3 tail floats on lanes 4..6
+    const int head = (int)(a0 - gs), t0 = (int)(a1 - gs);
+    const int e = lane < 4 ? lane : t0 + lane - 4;
+    if (lane < 4 ? lane < head : (lane < 8 && e < count)) dst[gs + e] = stage[pad + e];
   } else {
     for (int e = lane; e < count; e += 32) dst[gs + e] = stage[pad + e];
   }
+  // one (possibly empty) bulk group per flush keeps the double-buffer
+  // accounting exact: wait_group.read 1 frees the buffer before the last
+  if (lane == 0) bulk_commit();
 }
 
 // Position of the n-th (0-based) set bit of w, by popc halving.
@@ -143,23 +181,41 @@ __device__ __forceinline__ int nth_bit(uint32_t w, int n) {
 
 // Env b's observation rows and global-state row, one warp.  Rows are built
 // in shared memory R at a time (zero fill with 16-byte stores, then the own
-// block, the visible (observer, other) pair blocks enumerated from the N-bit
-// visibility rows, and the zone blocks) and leave through double-buffered
-// TMA bulk stores; hidden pairs -- most of the tensor -- cost only the fill.
+// block, the visible (observer, other) pair blocks, and the zone blocks) and
+// leave through double-buffered TMA bulk stores; hidden pairs -- most of the
+// tensor -- cost only the fill.  `buf` (the stage buffer to fill next)
+// persists across the envs a warp emits so the buffer rotation never waits
+// on the store just issued; drain = wait for every store before returning.
 template <int W>
-__device__ void emit_lane(const EmitEnv<W>& E, float* __restrict__ obs, float* __restrict__ glob,
-                          int64_t b, int N, int Z, int D, int G, int R, int SF, float* stage,
-                          const tabx_config* __restrict__ C, const DerivedCfg* __restrict__ DC,
-                          int lane) {
+__device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
+                          float* __restrict__ glob, int64_t b, int N, int Z, int D, int G, int R,
+                          int SF, const tabx_config* __restrict__ C,
+                          const DerivedCfg* __restrict__ DC, int lane, int& buf, bool drain) {
+  const EmitEnv<W>& E = X.E;
   const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
   const int M = N - 1;
   const int zoff = TABX_OWN_DIM + TABX_OTHER_DIM * M;
-  int buf = 0;
+  const int ZD = Z * TABX_ZONE_DIM;
+  // zone-block slots q = lane, lane + 32 of every active row: the template
+  // value and, for the two relative-position features of a used zone, the
+  // index into the row's zq entries (W == 1, ZD <= 64; else the generic loop)
+  const bool zfast = W == 1 && ZD <= 64;
+  float zt[2];
+  int zrel[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int q = lane + 32 * t;
+    zt[t] = q < ZD ? DC->zobs[q] : 0.0f;
+    const int z = q >> 3, f = q & 7;
+    zrel[t] = (q < ZD && (f == 3 || f == 4) && C->zone_type[z] != TABX_ZONE_NONE)
+                  ? 2 * z + (f - 3)
+                  : -1;
+  }
   if (obs) {
     for (int r0 = 0; r0 < N; r0 += R) {
       const int nr = min(R, N - r0);
       const int64_t gs = (b * N + r0) * (int64_t)D;
-      float* st = stage + buf * SF;
+      float* st = X.stage + buf * SF;
       const int pad = (int)(gs & 3);
       float* row0 = st + pad;
       if (lane == 0) bulk_wait_read<1>();
@@ -168,14 +224,10 @@ __device__ void emit_lane(const EmitEnv<W>& E, float* __restrict__ obs, float* _
         const int n4 = (pad + nr * D + 3) >> 2;
         float4* z4 = reinterpret_cast<float4*>(st);
         const float4 zero = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-        int q = lane;
-        for (; q + 96 < n4; q += 128) {
-          z4[q] = zero;
-          z4[q + 32] = zero;
-          z4[q + 64] = zero;
-          z4[q + 96] = zero;
-        }
-        for (; q < n4; q += 32) z4[q] = zero;
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (lane + 32 * t < n4) z4[lane + 32 * t] = zero;
+        for (int q = lane + 256; q < n4; q += 32) z4[q] = zero;
       }
       __syncwarp();
       for (int e = lane; e < nr * TABX_OWN_DIM; e += 32) {
@@ -183,31 +235,9 @@ __device__ void emit_lane(const EmitEnv<W>& E, float* __restrict__ obs, float* _
         row0[rr * D + f] = E.own[r0 + rr][f];
       }
       // visible pairs of the chunk's rows (vis excludes inactive rows/columns)
-      int total = 0;
-      for (int rr = 0; rr < nr; ++rr) {
-        const int r = r0 + rr;
-#pragma unroll
-        for (int k = 0; k < W; ++k)
-          total += __popc(E.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u));
-      }
-      for (int s = lane; s < total; s += 32) {
-        int rr = 0, n = s, j = -1;
-        for (; rr < nr; ++rr) {
-          const int r = r0 + rr;
-          for (int k = 0; k < W && j < 0; ++k) {
-            const uint32_t w = E.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u);
-            const int c = __popc(w);
-            if (n < c) {
-              j = (k << 5) + nth_bit(w, n);
-            } else {
-              n -= c;
-            }
-          }
-          if (j >= 0) break;
-        }
-        const int r = r0 + rr;
+      auto pair_block = [&](int r, int j) {
         const int kk = j - (j > r ? 1 : 0);
-        float* blk = row0 + rr * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
+        float* blk = row0 + (r - r0) * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
         const float4* oj = reinterpret_cast<const float4*>(E.own[j]);
         const float4 o0 = oj[0], o1 = oj[1], o2 = oj[2], o3 = oj[3];
         blk[0] = o0.x;
@@ -227,21 +257,76 @@ __device__ void emit_lane(const EmitEnv<W>& E, float* __restrict__ obs, float* _
         blk[14] = o3.z;
         blk[15] = (E.flags[j] & 2u) ? 1.0f : 0.0f;
         blk[16] = row_bit(&E.atk[r * W], j) ? 1.0f : 0.0f;
-      }
-      // zone blocks: lane z of each active row (unused slots stay zero)
-      if (lane < Z) {
-        const int z = lane;
-        const int ty = C->zone_type[z];
-        for (int rr = 0; rr < nr && ty != TABX_ZONE_NONE; ++rr) {
+      };
+      if constexpr (W == 1) {
+        // compact the chunk's visible pairs (row-major) with ballots
+        int cnt = 0;
+        const uint32_t lt = (1u << lane) - 1u;
+        for (int rr = 0; rr < nr; ++rr) {
           const int r = r0 + rr;
-          if (!(E.flags[r] & 1u)) continue;
-          float* zb = row0 + rr * D + zoff + TABX_ZONE_DIM * z;
-          zb[ty - 1] = 1.0f;
-          zb[3] = f32_quot(C->zone_cx[z] - E.px[r], fw, rw);
-          zb[4] = f32_quot(C->zone_cy[z] - E.py[r], fh, rh);
-          zb[5] = __double2float_rn(C->zone_ax[z]);
-          zb[6] = __double2float_rn(C->zone_ay[z]);
-          zb[7] = __double2float_rn(C->zone_effect[z]);
+          const uint32_t w = E.vis[r] & ~(1u << r);
+          if ((w >> lane) & 1u) X.clist[cnt + __popc(w & lt)] = (uint16_t)((rr << 5) | lane);
+          cnt += __popc(w);
+        }
+        __syncwarp();
+        for (int p = lane; p < cnt; p += 32) {
+          const int rj = X.clist[p];
+          pair_block(r0 + (rj >> 5), rj & 31);
+        }
+      } else {
+        int total = 0;
+        for (int rr = 0; rr < nr; ++rr) {
+          const int r = r0 + rr;
+#pragma unroll
+          for (int k = 0; k < W; ++k)
+            total += __popc(E.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u));
+        }
+        for (int s = lane; s < total; s += 32) {
+          int rr = 0, n = s, j = -1;
+          for (; rr < nr; ++rr) {
+            const int r = r0 + rr;
+            for (int k = 0; k < W && j < 0; ++k) {
+              const uint32_t w = E.vis[r * W + k] & ~(k == (r >> 5) ? 1u << (r & 31) : 0u);
+              const int c = __popc(w);
+              if (n < c) {
+                j = (k << 5) + nth_bit(w, n);
+              } else {
+                n -= c;
+              }
+            }
+            if (j >= 0) break;
+          }
+          pair_block(r0 + rr, j);
+        }
+      }
+      // zone blocks of the active rows: the config's template with the
+      // observer-relative position (unused zone slots stay zero)
+      for (int rr = 0; rr < nr; ++rr) {
+        const int r = r0 + rr;
+        if (!(E.flags[r] & 1u)) continue;
+        float* zb = row0 + rr * D + zoff;
+        if (zfast) {
+          const float* zr = reinterpret_cast<const float*>(X.zq) + 2 * r * Z;
+#pragma unroll
+          for (int t = 0; t < 2; ++t)
+            if (lane + 32 * t < ZD) zb[lane + 32 * t] = zrel[t] >= 0 ? zr[zrel[t]] : zt[t];
+          continue;
+        }
+        for (int q = lane; q < ZD; q += 32) {
+          const int z = q >> 3, f = q & 7;
+          float v = DC->zobs[q];
+          if (f == 3 || f == 4) {
+            if (C->zone_type[z] != TABX_ZONE_NONE) {
+              if constexpr (W == 1) {
+                const float2 zr = X.zq[r * Z + z];
+                v = f == 3 ? zr.x : zr.y;
+              } else {
+                v = f == 3 ? f32_quot(C->zone_cx[z] - E.px[r], fw, rw)
+                           : f32_quot(C->zone_cy[z] - E.py[r], fh, rh);
+              }
+            }
+          }
+          zb[q] = v;
         }
       }
       fence_proxy_async();
@@ -252,7 +337,7 @@ __device__ void emit_lane(const EmitEnv<W>& E, float* __restrict__ obs, float* _
   }
   if (glob) {
     const int64_t gs = b * (int64_t)G;
-    float* st = stage + buf * SF;
+    float* st = X.stage + buf * SF;
     float* row = st + (int)(gs & 3);
     if (lane == 0) bulk_wait_read<1>();
     __syncwarp();
@@ -260,30 +345,16 @@ __device__ void emit_lane(const EmitEnv<W>& E, float* __restrict__ obs, float* _
       const int u = e / TABX_OWN_DIM;
       row[e] = E.own[u][e - u * TABX_OWN_DIM];
     }
-    for (int q = lane; q < Z * TABX_ZONE_DIM; q += 32) {
-      const int z = q >> 3, f = q & 7;
-      const int ty = C->zone_type[z];
-      float v;
-      if (ty == TABX_ZONE_NONE) {
-        v = 0.0f;
-      } else {
-        switch (f) {
-          case 0: case 1: case 2: v = ty == f + 1 ? 1.0f : 0.0f; break;
-          case 3: v = f32_quot(C->zone_cx[z], fw, rw); break;
-          case 4: v = f32_quot(C->zone_cy[z], fh, rh); break;
-          case 5: v = __double2float_rn(C->zone_ax[z]); break;
-          case 6: v = __double2float_rn(C->zone_ay[z]); break;
-          default: v = __double2float_rn(C->zone_effect[z]); break;
-        }
-      }
-      row[N * TABX_OWN_DIM + q] = v;
-    }
+    for (int q = lane; q < ZD; q += 32) row[N * TABX_OWN_DIM + q] = DC->zglob[q];
     fence_proxy_async();
     __syncwarp();
     flush_stage(glob, gs, G, st, lane);
+    buf ^= 1;
   }
-  if (lane == 0) bulk_wait_read<0>();
-  __syncwarp();
+  if (drain) {
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+  }
 }
 
 // Stage geometry: R rows per chunk within `budget` bytes per buffer.
@@ -308,15 +379,40 @@ __host__ __device__ __forceinline__ int emit_stage_floats(int N, int D, int G, i
 #ifndef TABX_EMIT_MIN_BLOCKS
 #define TABX_EMIT_MIN_BLOCKS 3
 #endif
+// Bytes of one warp's emitter scratch (view, zone-relative table, stages).
+template <int W>
+__host__ __device__ __forceinline__ size_t emit_warp_bytes(int N, int Z, int R, int SF) {
+  return emit_view_bytes<W>(N) + emit_aux_bytes<W>(N, Z, R) + (size_t)2 * SF * sizeof(float);
+}
+template <int W>
+__device__ __forceinline__ EmitScratch<W> emit_scratch(unsigned char* base, int N, int Z, int R) {
+  EmitScratch<W> X;
+  unsigned char* p = base;
+  X.E.px = reinterpret_cast<double*>(p);
+  X.E.py = X.E.px + N;
+  p += align16((size_t)16 * N);
+  X.E.own = reinterpret_cast<float(*)[16]>(p);
+  p += (size_t)64 * N;
+  X.E.vis = reinterpret_cast<uint32_t*>(p);
+  X.E.atk = X.E.vis + N * W;
+  X.E.flags = X.E.atk + N * W;
+  p += align16((size_t)4 * N * (2 * W + 1));
+  X.zq = reinterpret_cast<float2*>(p);
+  X.clist = reinterpret_cast<uint16_t*>(p + (size_t)N * Z * sizeof(float2));
+  X.stage = reinterpret_cast<float*>(p + emit_aux_bytes<W>(N, Z, R));
+  return X;
+}
+
 template <int W, int EPW>
 __global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS)
     emit_kernel(const Params P, int R, int SF) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  EmitEnv<W>* views = reinterpret_cast<EmitEnv<W>*>(smem_raw);
-  float* stages = reinterpret_cast<float*>(smem_raw + ((sizeof(EmitEnv<W>) * EPW + 15) & ~15));
   if (P.mode == MODE_STEP && P.sync->err_index != NO_ERROR) return;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const EmitScratch<W> X =
+      emit_scratch<W>(smem_raw + (size_t)w * emit_warp_bytes<W>(P.N, P.Z, R, SF), P.N, P.Z, R);
   const DevState& st = P.st;
+  int buf = 0;
   for (int64_t b = (int64_t)blockIdx.x * EPW + w; b < P.B; b += (int64_t)gridDim.x * EPW) {
     const int32_t k = st.cfg[b];
     const tabx_config* C = P.cfgs + k;
@@ -325,9 +421,8 @@ __global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS)
     float* ob = pending ? P.out.final_observations : P.out.observations;
     float* gb = pending ? P.out.final_global_state : P.out.global_state;
     if (!ob && !gb) continue;
-    load_view<W>(views[w], st, b, P.N, C, DC, lane);
-    emit_lane<W>(views[w], ob, gb, b, P.N, P.Z, P.D, P.G, R, SF, stages + (size_t)w * 2 * SF, C,
-                 DC, lane);
+    load_view<W>(X, st, b, P.N, P.Z, C, DC, lane);
+    emit_lane<W>(X, ob, gb, b, P.N, P.Z, P.D, P.G, R, SF, C, DC, lane, buf, false);
   }
   if (lane == 0) bulk_wait_all();
 }
@@ -336,8 +431,7 @@ template <int W, int EPW>
 cudaError_t launch_emit_t(const Params& P, int sm_count, cudaStream_t stream) {
   const int R = emit_rows(P.N, P.D, W == 1 ? TABX_EMIT_BUDGET : 8192);
   const int SF = emit_stage_floats(P.N, P.D, P.G, R);
-  const size_t smem = ((sizeof(EmitEnv<W>) * EPW + 15) & ~(size_t)15) +
-                      (size_t)EPW * 2 * SF * sizeof(float);
+  const size_t smem = (size_t)EPW * emit_warp_bytes<W>(P.N, P.Z, R, SF);
   static size_t cached_smem = 0;
   static int per_sm = 0;
   if (smem != cached_smem) {

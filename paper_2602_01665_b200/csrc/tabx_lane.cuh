@@ -585,7 +585,7 @@ __device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_conf
 // ---------------------------------------------------------------- lane ---
 template <int W>
 __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
-                         EmitEnv<W>* emit, bool refresh, uint32_t step_no) {
+                         unsigned char* emit, bool refresh, uint32_t step_no) {
   const int N = P.N, Z = P.Z;
   const bool valid = i < N;
   const int64_t u = b * N + i;
@@ -739,10 +739,11 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     if (emit && i < 32) {
       const int R = emit_rows(N, P.D, W == 1 ? TABX_EMIT_BUDGET : 8192);
       const int SF = emit_stage_floats(N, P.D, P.G, R);
-      float* stage = reinterpret_cast<float*>(emit + 1);
-      load_view<W>(*emit, st, b, N, C, DC, i);
-      emit_lane<W>(*emit, O.observations, O.global_state, b, N, Z, P.D, P.G, R, SF, stage, C, DC,
-                   i);
+      const EmitScratch<W> X = emit_scratch<W>(emit, N, Z, R);
+      int buf = 0;
+      load_view<W>(X, st, b, N, Z, C, DC, i);
+      emit_lane<W>(X, O.observations, O.global_state, b, N, Z, P.D, P.G, R, SF, C, DC, i, buf,
+                   true);
     }
     env_sync<W>();
     return;
@@ -1207,7 +1208,7 @@ template <int W>
 __host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
   const int R = emit_rows(P.N, P.D, W == 1 ? TABX_EMIT_BUDGET : 8192);
   const int SF = emit_stage_floats(P.N, P.D, P.G, R);
-  return ((sizeof(EmitEnv<W>) + 15) & ~(size_t)15) + (size_t)2 * SF * sizeof(float);
+  return emit_warp_bytes<W>(P.N, P.Z, R, SF);
 }
 
 #ifndef TABX_MIN_BLOCKS
@@ -1249,7 +1250,7 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
   for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB) {
     if (P.mode == MODE_RESET && !(P.st.flags[b] & F_PEND)) continue;  // env-uniform
     run_lane<W>(P, b, i, envs[g],
-                P.mode == MODE_RESET ? reinterpret_cast<EmitEnv<W>*>(view_base + g * view_bytes)
+                P.mode == MODE_RESET ? view_base + g * view_bytes
                                      : nullptr,
                 refresh, step_no);
   }
