@@ -230,6 +230,15 @@ int tabx_reset_env(tabx_handle* h, int64_t b, const tabx_config* config, uint64_
 int tabx_respawn_all(tabx_handle* h, const uint64_t* seeds, const int32_t* env_config);
 
 int tabx_export_state(tabx_handle* h, const tabx_state* dst);
+/*
+ * Trace gather (rollout.py:150-188 records): row k of
+ * dst (n_lanes rows, the tabx_state layout) <- lane lanes[k] (device int64
+ * [n_lanes]).  Asynchronous on the handle's stream; unlike tabx_export_state
+ * it never materialises a pending cache refresh, so it does not perturb the
+ * batch (vis/atk rows are the stored caches).
+ */
+int tabx_export_lanes(tabx_handle* h, const int64_t* lanes, int64_t n_lanes,
+                      const tabx_state* dst);
 int tabx_import_state(tabx_handle* h, const tabx_state* src);
 
 /* Synchronises the stream; reports (and with clear != 0 clears) the action error. */

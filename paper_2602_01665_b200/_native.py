@@ -100,6 +100,7 @@ def lib() -> ct.CDLL:
                                   ct.POINTER(TabxOutputs)]),
         "tabx_respawn_all": (_i32, [P, P, P]),
         "tabx_export_state": (_i32, [P, ct.POINTER(TabxState)]),
+        "tabx_export_lanes": (_i32, [P, P, ct.c_int64, ct.POINTER(TabxState)]),
         "tabx_import_state": (_i32, [P, ct.POINTER(TabxState)]),
         "tabx_get_error": (_i32, [P, ct.POINTER(TabxError), _i32]),
         "tabx_episode_stats": (_i32, [P, P, P, _i32]),

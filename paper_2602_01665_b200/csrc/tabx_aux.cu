@@ -102,41 +102,45 @@ __global__ void spawn_kernel(DevState st, const tabx_config* __restrict__ cfgs,
   }
 }
 
-__global__ void export_kernel(DevState st, tabx_state d, int64_t B, int N, int W) {
-  const int64_t n = B * N;
-  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-       u += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = u / N;
-    const int i = (int)(u - b * N);
+// Row k of the destination <- lane lanes[k] (lanes == nullptr: lane k).
+__global__ void export_kernel(DevState st, tabx_state d, const int64_t* __restrict__ lanes,
+                              int64_t rows, int N, int W) {
+  const int64_t n = rows * N;
+  for (int64_t du = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; du < n;
+       du += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = du / N;
+    const int i = (int)(du - k * N);
+    const int64_t b = lanes ? lanes[k] : k;
+    const int64_t u = b * N + i;
     if (i == 0) {
-      if (d.seed) d.seed[b] = st.seed[b];
-      if (d.episode) d.episode[b] = st.episode[b];
-      if (d.t) d.t[b] = st.t[b];
-      if (d.prev_gap) d.prev_gap[b] = st.prev_gap[b];
-      if (d.ep_return) d.ep_return[b] = st.ep_return[b];
-      if (d.done) d.done[b] = (st.flags[b] & F_DONE) ? 1 : 0;
-      if (d.terminated) d.terminated[b] = (st.flags[b] & F_TERM) ? 1 : 0;
-      if (d.truncated) d.truncated[b] = (st.flags[b] & F_TRUNC) ? 1 : 0;
-      if (d.winner) d.winner[b] = st.winner[b];
-      if (d.reason) d.reason[b] = st.reason[b];
-      if (d.first_kill) d.first_kill[b] = st.first_kill[b];
-      if (d.config) d.config[b] = st.cfg[b];
+      if (d.seed) d.seed[k] = st.seed[b];
+      if (d.episode) d.episode[k] = st.episode[b];
+      if (d.t) d.t[k] = st.t[b];
+      if (d.prev_gap) d.prev_gap[k] = st.prev_gap[b];
+      if (d.ep_return) d.ep_return[k] = st.ep_return[b];
+      if (d.done) d.done[k] = (st.flags[b] & F_DONE) ? 1 : 0;
+      if (d.terminated) d.terminated[k] = (st.flags[b] & F_TERM) ? 1 : 0;
+      if (d.truncated) d.truncated[k] = (st.flags[b] & F_TRUNC) ? 1 : 0;
+      if (d.winner) d.winner[k] = st.winner[b];
+      if (d.reason) d.reason[k] = st.reason[b];
+      if (d.first_kill) d.first_kill[k] = st.first_kill[b];
+      if (d.config) d.config[k] = st.cfg[b];
     }
-    if (d.pos) { d.pos[2 * u] = st.pos[u].x; d.pos[2 * u + 1] = st.pos[u].y; }
-    if (d.heading) d.heading[u] = st.heading[u];
-    if (d.vel) { d.vel[2 * u] = st.vel[u].x; d.vel[2 * u + 1] = st.vel[u].y; }
-    if (d.imp_dv) { d.imp_dv[2 * u] = st.imp_dv[u].x; d.imp_dv[2 * u + 1] = st.imp_dv[u].y; }
-    if (d.health) d.health[u] = st.health[u];
-    if (d.cooldown) d.cooldown[u] = st.cooldown[u];
-    if (d.reveal) d.reveal[u] = st.reveal[u];
-    if (d.alive) d.alive[u] = (st.ubits[u] & U_ALIVE) ? 1 : 0;
-    if (d.mem_pos) { d.mem_pos[2 * u] = st.mem_pos[u].x; d.mem_pos[2 * u + 1] = st.mem_pos[u].y; }
-    if (d.mem_valid) d.mem_valid[u] = (st.ubits[u] & U_MEMV) ? 1 : 0;
+    if (d.pos) { d.pos[2 * du] = st.pos[u].x; d.pos[2 * du + 1] = st.pos[u].y; }
+    if (d.heading) d.heading[du] = st.heading[u];
+    if (d.vel) { d.vel[2 * du] = st.vel[u].x; d.vel[2 * du + 1] = st.vel[u].y; }
+    if (d.imp_dv) { d.imp_dv[2 * du] = st.imp_dv[u].x; d.imp_dv[2 * du + 1] = st.imp_dv[u].y; }
+    if (d.health) d.health[du] = st.health[u];
+    if (d.cooldown) d.cooldown[du] = st.cooldown[u];
+    if (d.reveal) d.reveal[du] = st.reveal[u];
+    if (d.alive) d.alive[du] = (st.ubits[u] & U_ALIVE) ? 1 : 0;
+    if (d.mem_pos) { d.mem_pos[2 * du] = st.mem_pos[u].x; d.mem_pos[2 * du + 1] = st.mem_pos[u].y; }
+    if (d.mem_valid) d.mem_valid[du] = (st.ubits[u] & U_MEMV) ? 1 : 0;
     for (int j = 0; j < N; ++j) {
       const uint32_t vb = (st.vis[u * W + (j >> 5)] >> (j & 31)) & 1u;
       const uint32_t ab = (st.atk[u * W + (j >> 5)] >> (j & 31)) & 1u;
-      if (d.vis) d.vis[u * N + j] = (uint8_t)vb;
-      if (d.atk) d.atk[u * N + j] = (uint8_t)ab;
+      if (d.vis) d.vis[du * N + j] = (uint8_t)vb;
+      if (d.atk) d.atk[du * N + j] = (uint8_t)ab;
     }
   }
 }
@@ -324,9 +328,10 @@ cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const Deri
   return cudaGetLastError();
 }
 
-cudaError_t launch_export(const DevState& st, const tabx_state& d, int64_t B, int N, int W,
-                          int sm_count, cudaStream_t stream) {
-  export_kernel<<<grid_for(B * N, 256, sm_count), 256, 0, stream>>>(st, d, B, N, W);
+cudaError_t launch_export(const DevState& st, const tabx_state& d, const int64_t* lanes,
+                          int64_t rows, int N, int W, int sm_count, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  export_kernel<<<grid_for(rows * N, 256, sm_count), 256, 0, stream>>>(st, d, lanes, rows, N, W);
   return cudaGetLastError();
 }
 

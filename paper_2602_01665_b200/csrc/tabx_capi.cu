@@ -20,8 +20,8 @@ cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const Deri
                          cudaStream_t stream);
 cudaError_t launch_derive(const tabx_config* cfgs, DerivedCfg* dcfgs, int k0, int k1,
                           cudaStream_t stream);
-cudaError_t launch_export(const DevState& st, const tabx_state& d, int64_t B, int N, int W,
-                          int sm_count, cudaStream_t stream);
+cudaError_t launch_export(const DevState& st, const tabx_state& d, const int64_t* lanes,
+                          int64_t rows, int N, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_import(const DevState& st, const tabx_state& s, const tabx_config* cfgs,
                           const DerivedCfg* dcfgs, int64_t B, int N, int W, int sm_count,
                           cudaStream_t stream);
@@ -431,7 +431,18 @@ int tabx_export_state(tabx_handle* h, const tabx_state* dst) {
   // caches pending a batch refresh are materialised first (refresh_caches)
   Params P = make_params(h, MODE_REFRESH, nullptr, nullptr);
   TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "refresh launch");
-  TABX_CUDA(launch_export(h->st, *dst, h->B, h->N, h->W, h->sm_count, h->stream), "export");
+  TABX_CUDA(launch_export(h->st, *dst, nullptr, h->B, h->N, h->W, h->sm_count, h->stream),
+            "export");
+  return TABX_OK;
+}
+
+int tabx_export_lanes(tabx_handle* h, const int64_t* lanes, int64_t n_lanes,
+                      const tabx_state* dst) {
+  if (!h || !dst || n_lanes < 0 || (n_lanes > 0 && !lanes))
+    return fail(TABX_E_ARGUMENT, "tabx_export_lanes: bad argument");
+  DeviceGuard guard(h->device);
+  TABX_CUDA(launch_export(h->st, *dst, lanes, n_lanes, h->N, h->W, h->sm_count, h->stream),
+            "export lanes");
   return TABX_OK;
 }
 

@@ -281,6 +281,26 @@ class BatchSim:
         torch.cuda.current_stream(self.device).synchronize()
         return out
 
+    def export_lanes(self, lanes: torch.Tensor, fields=None) -> dict[str, torch.Tensor]:
+        """State rows of ``lanes`` (device int64) for ``fields`` (default all),
+        gathered on the simulator's stream without synchronising and without
+        materialising a pending cache refresh (the trace gather)."""
+        L = nat.lib()
+        N = self.n_units
+        lanes = lanes.to(device=self.device, dtype=torch.int64).contiguous()
+        n = lanes.numel()
+        out = {}
+        for k in (fields or STATE_DTYPES):
+            dt, tail = STATE_DTYPES[k]
+            shape = (n,) if k in PER_LANE else (n, N) + tuple(N if x == "N" else x for x in tail)
+            out[k] = torch.empty(shape, dtype=dt, device=self.device)
+        st = nat.TabxState(*[_ptr(out.get(k)) for k in nat.STATE_FIELDS])
+        with torch.cuda.device(self.device):
+            nat.check(L.tabx_export_lanes(self._h, _ptr(lanes), n, ct.byref(st)),
+                      "tabx_export_lanes")
+        self._keep_lanes = lanes
+        return out
+
     def import_state(self, state: dict) -> None:
         """Overwrite dynamic state (parity injection); missing keys are kept."""
         L = nat.lib()
