@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define TABX_ABI_VERSION 1
+#define TABX_ABI_VERSION 2
 
 #define TABX_MAX_UNITS 256
 #define TABX_MAX_ZONES 32
@@ -179,6 +179,43 @@ typedef struct tabx_error {
   int64_t action;
 } tabx_error;
 
+/*
+ * Level generation (scenario.py:563-826).
+ * tabx_pcg64 is numpy's PCG64 bit-generator state (bit_generator.state:
+ * 128-bit state and increment, has_uint32 / uinteger buffer).
+ * tabx_level_spec is a LevelGenSpec resolved on the host: open categories,
+ * the unit ranges in sorted-name order (attack_damage, max_health, speed),
+ * the zone types in spec order, the centre box, axis range, effect ranges
+ * indexed by TABX_ZONE_*, and the heuristic ranges.
+ */
+typedef struct tabx_pcg64 {
+  uint64_t state_hi, state_lo;
+  uint64_t inc_hi, inc_lo;
+  uint32_t has_uint32, uinteger;
+} tabx_pcg64;
+
+typedef struct tabx_level_spec {
+  int32_t open_units, open_zones, open_heuristic;
+  int32_t unit_open[3];
+  double unit_lo[3], unit_hi[3];
+  int32_t n_zone_types;
+  int32_t zone_types[3];
+  double box_x0, box_x1, box_y0, box_y1;
+  int32_t axis_open;
+  double axis_lo, axis_hi;
+  int32_t effect_open[4];
+  double effect_lo[4], effect_hi[4];
+  int32_t eps_open;
+  double eps_lo, eps_hi;
+  int32_t agg_open;
+  double agg_lo, agg_hi;
+} tabx_level_spec;
+
+#define TABX_LEVEL_SAMPLE 0    /* sample_level(spec, rng), scenario.py:696-747 */
+#define TABX_LEVEL_PERTURB 1   /* mutate_level(.., "perturb"), :773-812 */
+#define TABX_LEVEL_SWAP_AXES 2 /* mutate_level(.., "swap_axes"), :814-818 */
+#define TABX_LEVEL_RETYPE 3    /* mutate_level(.., "retype"), :819-826 */
+
 typedef struct tabx_handle tabx_handle;
 
 int tabx_abi_version(void);
@@ -262,8 +299,39 @@ int tabx_episode_stats(tabx_handle* h, double* dst_host, double* dst_device, int
 int tabx_set_profiling(tabx_handle* h, int32_t enable);
 int tabx_get_profile(tabx_handle* h, double* ms, int64_t* steps);
 
+/*
+ * Config table management.  The table starts with the configs given to
+ * tabx_create (plus those added by tabx_reset_env); tabx_reserve_configs
+ * grows its capacity (synchronises), tabx_num_configs reports count and
+ * capacity, tabx_get_config copies one row to the host (synchronises).
+ */
+int tabx_reserve_configs(tabx_handle* h, int32_t capacity);
+int tabx_num_configs(tabx_handle* h, int32_t* count, int32_t* capacity);
+int tabx_get_config(tabx_handle* h, int32_t slot, tabx_config* dst);
+
+/*
+ * A batch of levels on the device, one per entry k < count: row
+ * dst_first + k of the config table <- op applied to row src_slots[k]
+ * (device int32 [count]; NULL = in place), drawing from rngs[k] (device
+ * tabx_pcg64 [count], advanced in place exactly as numpy's generator would
+ * be).  Source rows must not be destination rows of other entries.  The
+ * table grows to dst_first + count rows (within the capacity).  Async.
+ */
+int tabx_levels(tabx_handle* h, int32_t op, const tabx_level_spec* spec, double delta,
+                const int32_t* src_slots, int32_t dst_first, int32_t count, tabx_pcg64* rngs);
+
+/*
+ * Respawn lanes lanes[k] (device int64 [n]), first switching them to config
+ * slots[k] (device int32, may be NULL) and seeds[k] (device uint64, may be
+ * NULL): fill_env for a lane list (arrays.py:244-321).  Follow with
+ * tabx_init_output, as reset_env does (environment.py:490-498).  Async.
+ */
+int tabx_respawn_lanes(tabx_handle* h, const int64_t* lanes, const int32_t* slots,
+                       const uint64_t* seeds, int64_t n);
+
 /* sizeof of the ABI structs, so bindings can check their mirrors. */
-int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state);
+int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state, int64_t* level_spec,
+                      int64_t* pcg64);
 
 /* Test hook: libm-equal sin/cos of n device doubles (tabx_math.cuh). */
 int tabx_debug_sincos(const double* x, double* s, double* c, int64_t n, void* stream);

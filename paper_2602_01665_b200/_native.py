@@ -12,7 +12,7 @@ MAX_UNITS = 256
 MAX_ZONES = 32
 NUM_ACTIONS = 7
 NUM_STATS = 8
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 OK = 0
 E_ARGUMENT, E_CUDA, E_ACTION_MASK, E_SHAPE, E_ALIGNMENT, E_CAPACITY = 1, 2, 3, 4, 5, 6
@@ -66,6 +66,28 @@ class TabxState(ct.Structure):
     _fields_ = [(name, ct.c_void_p) for name in STATE_FIELDS]
 
 
+class TabxPcg64(ct.Structure):
+    """numpy PCG64 bit-generator state (tabx.h)."""
+    _fields_ = [("state_hi", ct.c_uint64), ("state_lo", ct.c_uint64), ("inc_hi", ct.c_uint64),
+                ("inc_lo", ct.c_uint64), ("has_uint32", ct.c_uint32), ("uinteger", ct.c_uint32)]
+
+
+class TabxLevelSpec(ct.Structure):
+    _fields_ = [
+        ("open_units", _i32), ("open_zones", _i32), ("open_heuristic", _i32),
+        ("unit_open", _i32 * 3), ("unit_lo", _d * 3), ("unit_hi", _d * 3),
+        ("n_zone_types", _i32), ("zone_types", _i32 * 3),
+        ("box_x0", _d), ("box_x1", _d), ("box_y0", _d), ("box_y1", _d),
+        ("axis_open", _i32), ("axis_lo", _d), ("axis_hi", _d),
+        ("effect_open", _i32 * 4), ("effect_lo", _d * 4), ("effect_hi", _d * 4),
+        ("eps_open", _i32), ("eps_lo", _d), ("eps_hi", _d),
+        ("agg_open", _i32), ("agg_lo", _d), ("agg_hi", _d),
+    ]
+
+
+LEVEL_SAMPLE, LEVEL_PERTURB, LEVEL_SWAP_AXES, LEVEL_RETYPE = 0, 1, 2, 3
+
+
 class TabxError(ct.Structure):
     _fields_ = [("code", _i32), ("unit", _i32), ("env", _i64), ("action", _i64)]
 
@@ -104,7 +126,12 @@ def lib() -> ct.CDLL:
         "tabx_import_state": (_i32, [P, ct.POINTER(TabxState)]),
         "tabx_get_error": (_i32, [P, ct.POINTER(TabxError), _i32]),
         "tabx_episode_stats": (_i32, [P, P, P, _i32]),
-        "tabx_struct_sizes": (_i32, [P, P, P]),
+        "tabx_struct_sizes": (_i32, [P, P, P, P, P]),
+        "tabx_reserve_configs": (_i32, [P, _i32]),
+        "tabx_num_configs": (_i32, [P, P, P]),
+        "tabx_get_config": (_i32, [P, _i32, ct.POINTER(TabxConfig)]),
+        "tabx_levels": (_i32, [P, _i32, ct.POINTER(TabxLevelSpec), _d, P, _i32, _i32, P]),
+        "tabx_respawn_lanes": (_i32, [P, P, P, P, _i64]),
         "tabx_set_profiling": (_i32, [P, _i32]),
         "tabx_get_profile": (_i32, [P, P, P]),
         "tabx_debug_sincos": (_i32, [P, P, P, _i64, P]),
@@ -115,9 +142,10 @@ def lib() -> ct.CDLL:
         fn.argtypes = args
     if L.tabx_abi_version() != ABI_VERSION:
         raise ImportError(f"{LIB_PATH}: ABI {L.tabx_abi_version()} != {ABI_VERSION}")
-    sizes = [_i64(), _i64(), _i64()]
+    sizes = [_i64() for _ in range(5)]
     L.tabx_struct_sizes(*[ct.byref(s) for s in sizes])
-    mine = (ct.sizeof(TabxConfig), ct.sizeof(TabxOutputs), ct.sizeof(TabxState))
+    mine = (ct.sizeof(TabxConfig), ct.sizeof(TabxOutputs), ct.sizeof(TabxState),
+            ct.sizeof(TabxLevelSpec), ct.sizeof(TabxPcg64))
     if tuple(s.value for s in sizes) != mine:
         raise ImportError(f"{LIB_PATH}: struct layout mismatch {sizes} vs {mine}")
     _LIB = L

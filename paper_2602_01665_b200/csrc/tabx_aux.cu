@@ -56,10 +56,21 @@ __global__ void validate_kernel(const int64_t* __restrict__ actions, DevState st
 }
 
 // fill_env for lanes [b0, b1) (arrays.py:244-321); also used at creation.
+// With a lane list, entry k spawns lane lanes[k], first switching it to
+// config slots[k] and seed seeds[k] when those are given.
 __global__ void spawn_kernel(DevState st, const tabx_config* __restrict__ cfgs,
                              const DerivedCfg* __restrict__ dcfgs, int64_t b0, int64_t b1, int N,
-                             int W, int reset_stats) {
-  for (int64_t b = b0 + blockIdx.x; b < b1; b += gridDim.x) {
+                             int W, int reset_stats, const int64_t* __restrict__ lanes,
+                             const int32_t* __restrict__ slots, const uint64_t* __restrict__ seeds) {
+  for (int64_t k = b0 + blockIdx.x; k < b1; k += gridDim.x) {
+    const int64_t b = lanes ? lanes[k] : k;
+    if (slots || seeds) {
+      if (threadIdx.x == 0) {
+        if (slots) st.cfg[b] = slots[k];
+        if (seeds) st.seed[b] = seeds[k];
+      }
+      __syncthreads();
+    }
     const tabx_config* C = cfgs + st.cfg[b];
     const DerivedCfg* DC = dcfgs + st.cfg[b];
     for (int i = threadIdx.x; i < N; i += blockDim.x) {
@@ -324,7 +335,18 @@ cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const Deri
   int64_t n = b1 - b0;
   int grid = (int)(n < (int64_t)sm_count * 32 ? n : (int64_t)sm_count * 32);
   if (grid < 1) return cudaSuccess;
-  spawn_kernel<<<grid, 32 * W, 0, stream>>>(st, cfgs, dcfgs, b0, b1, N, W, reset_stats);
+  spawn_kernel<<<grid, 32 * W, 0, stream>>>(st, cfgs, dcfgs, b0, b1, N, W, reset_stats, nullptr,
+                                             nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spawn_lanes(const DevState& st, const tabx_config* cfgs,
+                               const DerivedCfg* dcfgs, const int64_t* lanes, const int32_t* slots,
+                               const uint64_t* seeds, int64_t n, int N, int W, int sm_count,
+                               cudaStream_t stream) {
+  int grid = (int)(n < (int64_t)sm_count * 32 ? n : (int64_t)sm_count * 32);
+  if (grid < 1) return cudaSuccess;
+  spawn_kernel<<<grid, 32 * W, 0, stream>>>(st, cfgs, dcfgs, 0, n, N, W, 0, lanes, slots, seeds);
   return cudaGetLastError();
 }
 

@@ -20,6 +20,13 @@ cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const Deri
                          cudaStream_t stream);
 cudaError_t launch_derive(const tabx_config* cfgs, DerivedCfg* dcfgs, int k0, int k1,
                           cudaStream_t stream);
+cudaError_t launch_levels(tabx_config* cfgs, const int32_t* src_slots, int32_t dst_first,
+                          int32_t count, const tabx_level_spec& spec, int op, double delta,
+                          tabx_pcg64* rngs, int sm_count, cudaStream_t stream);
+cudaError_t launch_spawn_lanes(const DevState& st, const tabx_config* cfgs,
+                               const DerivedCfg* dcfgs, const int64_t* lanes, const int32_t* slots,
+                               const uint64_t* seeds, int64_t n, int N, int W, int sm_count,
+                               cudaStream_t stream);
 cudaError_t launch_export(const DevState& st, const tabx_state& d, const int64_t* lanes,
                           int64_t rows, int N, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_import(const DevState& st, const tabx_state& s, const tabx_config* cfgs,
@@ -41,7 +48,9 @@ struct tabx_handle {
   int auto_reset = 0;
   int sm_count = 148;
   bool any_external = false;
-  std::vector<tabx_config> cfg_host;
+  std::vector<tabx_config> cfg_host;  // host mirror of the table rows
+  std::vector<char> cfg_host_ok;       // 0: row written on the device (tabx_levels)
+  int cfg_cap = TABX_MAX_CONFIGS;
   tabx_config* cfg_dev = nullptr;
   DerivedCfg* dcfg_dev = nullptr;
   DevState st{};
@@ -140,14 +149,15 @@ static int find_or_add_config(tabx_handle* h, const tabx_config* c, int32_t* idx
   if (c->n_units != h->N || c->n_zones != h->Z)
     return fail(TABX_E_SHAPE, "batched environments must share max_units and max_zones");
   for (size_t k = 0; k < h->cfg_host.size(); ++k) {
-    if (!memcmp(&h->cfg_host[k], c, sizeof(tabx_config))) {
+    if (h->cfg_host_ok[k] && !memcmp(&h->cfg_host[k], c, sizeof(tabx_config))) {
       *idx = (int32_t)k;
       return TABX_OK;
     }
   }
-  if (h->cfg_host.size() >= TABX_MAX_CONFIGS)
+  if ((int)h->cfg_host.size() >= h->cfg_cap)
     return fail(TABX_E_CAPACITY, "config table full");
   h->cfg_host.push_back(*c);
+  h->cfg_host_ok.push_back(1);
   const size_t k = h->cfg_host.size() - 1;
   TABX_CUDA(cudaMemcpyAsync(h->cfg_dev + k, c, sizeof(tabx_config), cudaMemcpyHostToDevice,
                             h->stream),
@@ -268,6 +278,7 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   int rc = TABX_OK;
   for (int k = 0; k < n_configs; ++k) {
     h->cfg_host.push_back(configs[k]);
+    h->cfg_host_ok.push_back(1);
     if (configs[k].controller[0] == TABX_CTRL_EXTERNAL ||
         configs[k].controller[1] == TABX_CTRL_EXTERNAL)
       h->any_external = true;
@@ -446,6 +457,93 @@ int tabx_export_lanes(tabx_handle* h, const int64_t* lanes, int64_t n_lanes,
   return TABX_OK;
 }
 
+int tabx_reserve_configs(tabx_handle* h, int32_t capacity) {
+  if (!h || capacity < 1) return fail(TABX_E_ARGUMENT, "tabx_reserve_configs: bad argument");
+  if (capacity <= h->cfg_cap) return TABX_OK;
+  DeviceGuard guard(h->device);
+  tabx_config* c2 = nullptr;
+  DerivedCfg* d2 = nullptr;
+  cudaError_t e = cudaMalloc((void**)&c2, sizeof(tabx_config) * (size_t)capacity);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&d2, sizeof(DerivedCfg) * (size_t)capacity);
+  const size_t n = h->cfg_host.size();
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(c2, h->cfg_dev, sizeof(tabx_config) * n, cudaMemcpyDeviceToDevice,
+                        h->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d2, h->dcfg_dev, sizeof(DerivedCfg) * n, cudaMemcpyDeviceToDevice,
+                        h->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) {
+    cudaFree(c2);
+    cudaFree(d2);
+    return cuda_fail(e, "tabx_reserve_configs");
+  }
+  cudaFree(h->cfg_dev);
+  cudaFree(h->dcfg_dev);
+  h->cfg_dev = c2;
+  h->dcfg_dev = d2;
+  h->cfg_cap = capacity;
+  return TABX_OK;
+}
+
+int tabx_num_configs(tabx_handle* h, int32_t* count, int32_t* capacity) {
+  if (!h) return fail(TABX_E_ARGUMENT, "tabx_num_configs: bad argument");
+  if (count) *count = (int32_t)h->cfg_host.size();
+  if (capacity) *capacity = h->cfg_cap;
+  return TABX_OK;
+}
+
+int tabx_get_config(tabx_handle* h, int32_t slot, tabx_config* dst) {
+  if (!h || !dst || slot < 0 || slot >= (int32_t)h->cfg_host.size())
+    return fail(TABX_E_ARGUMENT, "tabx_get_config: bad argument");
+  DeviceGuard guard(h->device);
+  TABX_CUDA(cudaMemcpyAsync(dst, h->cfg_dev + slot, sizeof(tabx_config), cudaMemcpyDeviceToHost,
+                            h->stream),
+            "config read");
+  TABX_CUDA(cudaStreamSynchronize(h->stream), "config read sync");
+  return TABX_OK;
+}
+
+int tabx_levels(tabx_handle* h, int32_t op, const tabx_level_spec* spec, double delta,
+                const int32_t* src_slots, int32_t dst_first, int32_t count, tabx_pcg64* rngs) {
+  if (!h || !spec || count < 0 || (count > 0 && !rngs) || op < TABX_LEVEL_SAMPLE ||
+      op > TABX_LEVEL_RETYPE || spec->n_zone_types < 1 || spec->n_zone_types > 3)
+    return fail(TABX_E_ARGUMENT, "tabx_levels: bad argument");
+  if (dst_first < 0 || dst_first > (int32_t)h->cfg_host.size() ||
+      (int64_t)dst_first + count > h->cfg_cap)
+    return fail(TABX_E_CAPACITY, "tabx_levels: destination rows outside the config table");
+  for (int k = 0; k < spec->n_zone_types; ++k)
+    if (spec->zone_types[k] < TABX_ZONE_LAVA || spec->zone_types[k] > TABX_ZONE_SWAMP)
+      return fail(TABX_E_ARGUMENT, "tabx_levels: bad zone type");
+  if (count == 0) return TABX_OK;
+  DeviceGuard guard(h->device);
+  TABX_CUDA(launch_levels(h->cfg_dev, src_slots, dst_first, count, *spec, op, delta, rngs,
+                          h->sm_count, h->stream),
+            "levels");
+  TABX_CUDA(launch_derive(h->cfg_dev, h->dcfg_dev, dst_first, dst_first + count, h->stream),
+            "levels derive");
+  // rows written on the device: the host mirror no longer describes them
+  const size_t end = (size_t)dst_first + (size_t)count;
+  if (h->cfg_host.size() < end) {
+    h->cfg_host.resize(end);
+    h->cfg_host_ok.resize(end, 0);
+  }
+  for (size_t k = (size_t)dst_first; k < end; ++k) h->cfg_host_ok[k] = 0;
+  return TABX_OK;
+}
+
+int tabx_respawn_lanes(tabx_handle* h, const int64_t* lanes, const int32_t* slots,
+                       const uint64_t* seeds, int64_t n) {
+  if (!h || n < 0 || (n > 0 && !lanes))
+    return fail(TABX_E_ARGUMENT, "tabx_respawn_lanes: bad argument");
+  if (n == 0) return TABX_OK;
+  DeviceGuard guard(h->device);
+  TABX_CUDA(launch_spawn_lanes(h->st, h->cfg_dev, h->dcfg_dev, lanes, slots, seeds, n, h->N, h->W,
+                               h->sm_count, h->stream),
+            "respawn lanes");
+  return TABX_OK;
+}
+
 int tabx_import_state(tabx_handle* h, const tabx_state* src) {
   if (!h || !src) return fail(TABX_E_ARGUMENT, "tabx_import_state: bad argument");
   DeviceGuard guard(h->device);
@@ -523,10 +621,13 @@ int tabx_get_profile(tabx_handle* h, double* ms, int64_t* steps) {
   return TABX_OK;
 }
 
-int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state) {
+int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state, int64_t* level_spec,
+                      int64_t* pcg64) {
   if (config) *config = (int64_t)sizeof(tabx_config);
   if (outputs) *outputs = (int64_t)sizeof(tabx_outputs);
   if (state) *state = (int64_t)sizeof(tabx_state);
+  if (level_spec) *level_spec = (int64_t)sizeof(tabx_level_spec);
+  if (pcg64) *pcg64 = (int64_t)sizeof(tabx_pcg64);
   return TABX_OK;
 }
 

@@ -41,10 +41,11 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_struct_layouts_match(lib):
     from paper_2602_01665_b200 import _native as nat
-    sizes = [ct.c_int64(), ct.c_int64(), ct.c_int64()]
+    sizes = [ct.c_int64() for _ in range(5)]
     lib.tabx_struct_sizes(*[ct.byref(s) for s in sizes])
     assert [s.value for s in sizes] == [ct.sizeof(nat.TabxConfig), ct.sizeof(nat.TabxOutputs),
-                                        ct.sizeof(nat.TabxState)]
+                                        ct.sizeof(nat.TabxState), ct.sizeof(nat.TabxLevelSpec),
+                                        ct.sizeof(nat.TabxPcg64)]
 
 
 def test_dims_and_errors_without_gpu(lib):
