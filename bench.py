@@ -425,8 +425,8 @@ def main(argv=None) -> int:
     ap.add_argument("--envs", type=int, default=0, help="total environments (all ranks)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--cpu-envs", type=int, default=256)
-    ap.add_argument("--cpu-steps", type=int, default=40)
+    ap.add_argument("--cpu-envs", type=int, default=1024)
+    ap.add_argument("--cpu-steps", type=int, default=100)
     ap.add_argument("--cpu-workers", type=int, default=0, help="reference arm processes (0 = all cores)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
