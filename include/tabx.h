@@ -333,6 +333,12 @@ int tabx_respawn_lanes(tabx_handle* h, const int64_t* lanes, const int32_t* slot
 int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state, int64_t* level_spec,
                       int64_t* pcg64);
 
+/*
+ * Tool hook: SM cycles per step phase summed over envs (W = 1 step kernel),
+ * nonzero only in a build with -DTABX_PHASE_PROF (tools/phase_prof.py).
+ */
+int tabx_debug_phase_cycles(uint64_t* host16, int32_t reset);
+
 /* Test hook: libm-equal sin/cos of n device doubles (tabx_math.cuh). */
 int tabx_debug_sincos(const double* x, double* s, double* c, int64_t n, void* stream);
 

@@ -135,6 +135,7 @@ def lib() -> ct.CDLL:
         "tabx_set_profiling": (_i32, [P, _i32]),
         "tabx_get_profile": (_i32, [P, P, P]),
         "tabx_debug_sincos": (_i32, [P, P, P, _i64, P]),
+        "tabx_debug_phase_cycles": (_i32, [P, _i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

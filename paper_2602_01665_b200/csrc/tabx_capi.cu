@@ -27,6 +27,7 @@ cudaError_t launch_spawn_lanes(const DevState& st, const tabx_config* cfgs,
                                const DerivedCfg* dcfgs, const int64_t* lanes, const int32_t* slots,
                                const uint64_t* seeds, int64_t n, int N, int W, int sm_count,
                                cudaStream_t stream);
+cudaError_t phase_cycles_w1(unsigned long long* host16, int reset);
 cudaError_t launch_export(const DevState& st, const tabx_state& d, const int64_t* lanes,
                           int64_t rows, int N, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_import(const DevState& st, const tabx_state& s, const tabx_config* cfgs,
@@ -628,6 +629,12 @@ int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state, int64_t
   if (state) *state = (int64_t)sizeof(tabx_state);
   if (level_spec) *level_spec = (int64_t)sizeof(tabx_level_spec);
   if (pcg64) *pcg64 = (int64_t)sizeof(tabx_pcg64);
+  return TABX_OK;
+}
+
+int tabx_debug_phase_cycles(uint64_t* host16, int32_t reset) {
+  if (!host16) return fail(TABX_E_ARGUMENT, "tabx_debug_phase_cycles: bad argument");
+  TABX_CUDA(phase_cycles_w1((unsigned long long*)host16, reset), "phase cycles");
   return TABX_OK;
 }
 

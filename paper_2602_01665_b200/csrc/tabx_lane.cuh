@@ -45,6 +45,29 @@ __device__ __forceinline__ double uniform53(uint64_t seed, uint64_t step, uint64
   return (double)(key_hash(seed, step, tag, lane) >> 11) * (1.0 / 9007199254740992.0);
 }
 
+// ------------------------------------------------- phase instrumentation --
+// Built only with -DTABX_PHASE_PROF (tools): lane 0 of each env accumulates
+// SM clock cycles per step phase into tabx_phase_cycles (read back with
+// tabx_debug_phase_cycles).  The default build compiles the marks to nothing.
+#ifdef TABX_PHASE_PROF
+__device__ unsigned long long tabx_phase_cycles[16];
+#define TABX_PHASE_BEGIN() long long ph_t0_ = clock64()
+#define TABX_PHASE(k)                                                  \
+  do {                                                                 \
+    const long long ph_t1_ = clock64();                                \
+    if ((threadIdx.x & 31) == 0)                                       \
+      atomicAdd(&tabx_phase_cycles[k], (unsigned long long)(ph_t1_ - ph_t0_)); \
+    ph_t0_ = ph_t1_;                                                   \
+  } while (0)
+#else
+#define TABX_PHASE_BEGIN() \
+  do {                     \
+  } while (0)
+#define TABX_PHASE(k) \
+  do {                \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------- helpers --
 constexpr uint32_t UF_ACTIVE = 1, UF_ALIVE = 2, UF_ENEMY = 4, UF_KIN = 8, UF_INJURED = 16;
 
@@ -597,6 +620,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const double dt = C->dt, fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
   const double rmh = valid ? DC->rmh[i] : 1.0, rucd = valid ? DC->rucd[i] : 0.0;
 
+  TABX_PHASE_BEGIN();
   // ---- lane + unit state
   uint8_t lf = st.flags[b];
   const bool running = !(lf & F_DONE);
@@ -817,12 +841,14 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
   env_sync<W>();
 
+  TABX_PHASE(0);
   // 1. pre-step action mask (arrays.py:373-387)
   const bool ctl = alive && U.active;
   const uint32_t mask7 = ctl ? (0x1Fu | ((cd <= 0.0) ? 0x20u : 0u) | (C->enable_noop ? 0x40u : 0u))
                              : 0x40u;
   // effective speed after swamps at the pre-move position (arrays.py:338-343)
   const double speff = U.speed * swamp_mult(C, Z, S.zin[i], swamp_m);
+  TABX_PHASE(9);
   // 2. action resolution (environment.py:154-204)
   const int team = U.enemy ? 1 : 0;
   const int ctrl = C->controller[team];
@@ -849,6 +875,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 #pragma unroll
       for (int k = 0; k < W; ++k) vis[k] = atk[k] = 0u;
     }
+    TABX_PHASE(10);
     if (heur) {
       if (!refresh) {  // the refreshed rows are already in S.vis / S.atk
 #pragma unroll
@@ -870,11 +897,13 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
       }
       memv = (r & (SA_HAS | SA_MEMOK)) != 0;
     }
+    TABX_PHASE(11);
   }
   if (free_u && ctrl == TABX_CTRL_RANDOM)
     act = kth_legal(mask7, uniform53(seed, (uint64_t)(int64_t)t, TAG_RANDOM, (uint64_t)i));
   if (!free_u) act = A_NOOP;
 
+  TABX_PHASE(1);
   // 3-4. commanded velocity, integration, timers (environment.py:215-228)
   const bool moving = act < 4 && alive && U.active && !U.kin;
   const double vmag = moving ? speff : 0.0;
@@ -1027,6 +1056,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     vly = vfy;
   }
 
+  TABX_PHASE(2);
   // 6. boundary penalty + clip (physics.py:97-120)
   if (running && valid) {
     const bool out = px < 0.0 || px > fw || py < 0.0 || py > fh;
@@ -1046,12 +1076,15 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     }
   }
 
+  TABX_PHASE(3);
   // 8. caches at the post-move state (environment.py:254-257)
   zin = valid ? zone_bits(C, DC, Z, px, py) : 0u;
+  TABX_PHASE(12);
   env_sync<W>();
   publish();
-    build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
+  build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
   env_sync<W>();
+  TABX_PHASE(13);
   tgt = cache_row_inl<W>(S, i, N, U, bush_m);
 #pragma unroll
   for (int k = 0; k < W; ++k) {
@@ -1059,6 +1092,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     atk[k] = S.atk[i * W + k];
   }
 
+  TABX_PHASE(4);
   // 9. combat (combat.py:86-113; environment.py:259-265)
   const bool swing = act == A_ATTACK && alive && U.active && cd <= 0.0;
   const bool landed = running && swing && tgt >= 0;
@@ -1098,6 +1132,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const bool ally_died = env_any<W>(died && !U.enemy, S, i);
   if (any_died && fk < 0) fk = ally_died ? ENEMY : ALLY;
 
+  TABX_PHASE(5);
   // rewards and termination (environment.py:288-328)
   double ra, re;
   team_ratios<W>(S, i, N, U.active, U.enemy, hp, U.mh, n_ally, n_enemy, ra, re);
@@ -1133,6 +1168,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const double reward_i =
       ((U.enemy ? -1.0 : 1.0) * (U.active ? 1.0 : 0.0)) * (running ? ally_reward : 0.0);
 
+  TABX_PHASE(6);
   // ---- outputs of this step (observation uses stage-8 caches, post-step state)
   const tabx_outputs& O = P.out;
   const bool resets = P.auto_reset && (lf & F_DONE);
@@ -1172,6 +1208,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     }
   }
 
+  TABX_PHASE(7);
   // ---- state write-back
   if (valid) {
     st.pos[u] = make_double2(px, py);
@@ -1200,6 +1237,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     st.reason[b] = (int8_t)reason;
     st.first_kill[b] = (int8_t)fk;
   }
+  TABX_PHASE(8);
   env_sync<W>();
 }
 
