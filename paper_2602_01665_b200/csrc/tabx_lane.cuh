@@ -495,8 +495,13 @@ __device__ __forceinline__ void team_ratios(EnvSmem<W>& S, int i, int N, bool ac
 // Heuristic opponent decision for unit i (heuristics.py:103-243).
 // Returns the action packed with the scripted-controller memory update.
 constexpr int SA_ACT_MASK = 0xff, SA_HAS = 0x100, SA_MEMOK = 0x200, SA_TGT_SHIFT = 16;
+#ifdef TABX_INLINE_SCRIPTED
+#define TABX_SCRIPTED_QUAL __device__ __forceinline__
+#else
+#define TABX_SCRIPTED_QUAL __device__ __noinline__
+#endif
 template <int W>
-__device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
+TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
                                int N, int Z, double hd, double cd, double step,
                                uint32_t mask7, double u_explore, uint64_t seed, uint64_t t_step,
                                double eps, double xi, uint32_t bush_m, double mx, double my,
@@ -606,7 +611,7 @@ __device__ __noinline__ int scripted_action(const EnvSmem<W>& S, const tabx_conf
 }
 
 // ---------------------------------------------------------------- lane ---
-template <int W>
+template <int W, int M>
 __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
                          unsigned char* emit, bool refresh, uint32_t step_no) {
   const int N = P.N, Z = P.Z;
@@ -648,7 +653,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     ivy = iv.y;
     // realized velocity is output-only (written back only by running lanes);
     // the scripted-controller memory only exists for heuristic-team units
-    if (P.mode == MODE_STEP && C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC) {
+    if (M == MODE_STEP && C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC) {
       const double2 m = st.mem_pos[u];
       mx = m.x;
       my = m.y;
@@ -681,7 +686,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   uint32_t vis[W], atk[W];
   int tgt = -1;
 
-  if (P.mode == MODE_RESET) {
+  if (M == MODE_RESET) {
     // deferred auto-reset of a finished lane (environment.py:502-517): reseed,
     // respawn from the config template, fresh caches and prev_gap, then the
     // fresh observation / mask replace the step's (final ones were written by
@@ -773,12 +778,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     return;
   }
 
-  if (P.mode != MODE_STEP) {
+  if (M != MODE_STEP) {
     // init_output / refresh_caches (environment.py:147-151, :351-374)
     publish();
     build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
     env_sync<W>();
-    if (P.mode == MODE_REFRESH) {
+    if (M == MODE_REFRESH) {
       if (refresh) {
         cache_row_of<W>(S, i, N, U, bush_m);
         if (valid)
@@ -1253,7 +1258,9 @@ __host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
 #define TABX_MIN_BLOCKS 4
 #endif
 // K1 (MODE_STEP / MODE_INIT / MODE_REFRESH) and K3 (MODE_RESET).
-template <int W, int EPB>
+// One kernel per mode (M): the step kernel carries no reset / emitter code,
+// which keeps its instruction footprint and register allocation to its own.
+template <int W, int EPB, int M>
 __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
     lane_kernel(const Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1264,13 +1271,13 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
 
   uint32_t step_no = 0;
   bool refresh = false;
-  if (P.mode == MODE_STEP || P.mode == MODE_RESET) {
+  if (M == MODE_STEP || M == MODE_RESET) {
     if (P.sync->err_index != NO_ERROR) return;  // an action violated the mask: no mutation
     step_no = P.sync->step;
     refresh = P.sync->refresh[step_no % 3] != 0;
-    if (P.mode == MODE_STEP && blockIdx.x == 0 && threadIdx.x == 0)
+    if (M == MODE_STEP && blockIdx.x == 0 && threadIdx.x == 0)
       P.sync->refresh[(step_no + 2) % 3] = 0;
-  } else if (P.mode == MODE_REFRESH) {
+  } else if (M == MODE_REFRESH) {
     step_no = P.sync->step;
     refresh = P.sync->refresh[step_no % 3] != 0;
   }
@@ -1286,14 +1293,14 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
     __syncwarp();
   }
   for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB) {
-    if (P.mode == MODE_RESET && !(P.st.flags[b] & F_PEND)) continue;  // env-uniform
-    run_lane<W>(P, b, i, envs[g],
-                P.mode == MODE_RESET ? view_base + g * view_bytes
+    if (M == MODE_RESET && !(P.st.flags[b] & F_PEND)) continue;  // env-uniform
+    run_lane<W, M>(P, b, i, envs[g],
+                M == MODE_RESET ? view_base + g * view_bytes
                                      : nullptr,
                 refresh, step_no);
   }
 
-  if (P.mode == MODE_RESET) {
+  if (M == MODE_RESET) {
     // the reset kernel ends the step: advance the device step counter
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1309,34 +1316,45 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
 }
 
 // ------------------------------------------------------------ launchers --
-template <int W, int EPB>
-cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream, int* grid_out) {
+template <int W, int EPB, int M>
+cudaError_t launch_lanes_m(const Params& P, int sm_count, cudaStream_t stream, int* grid_out) {
   const int threads = 32 * W * EPB;
   const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
-  const size_t smem = env_bytes + (P.mode == MODE_RESET ? reset_view_bytes<W>(P) * EPB : 0);
+  const size_t smem = env_bytes + (M == MODE_RESET ? reset_view_bytes<W>(P) * EPB : 0);
   // attribute + occupancy are host-side queries; cache them per smem size so a
   // step costs one launch per kernel (and stays capturable in a CUDA graph)
-  static size_t cached_smem[2] = {0, 0};
-  static int cached_per_sm[2] = {0, 0};
-  const int slot = P.mode == MODE_RESET ? 1 : 0;
-  int per_sm = cached_per_sm[slot];
-  if (smem != cached_smem[slot]) {
-    cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB>,
+  static size_t cached_smem = 0;
+  static int cached_per_sm = 0;
+  int per_sm = cached_per_sm;
+  if (smem != cached_smem) {
+    cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB, M>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lane_kernel<W, EPB>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lane_kernel<W, EPB, M>, threads,
+                                                      smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
-    cached_smem[slot] = smem;
-    cached_per_sm[slot] = per_sm;
+    cached_smem = smem;
+    cached_per_sm = per_sm;
   }
   int64_t need = (P.B + EPB - 1) / EPB;
   int64_t cap = (int64_t)sm_count * per_sm;
   int grid = (int)(need < cap ? need : cap);
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
-  lane_kernel<W, EPB><<<grid, threads, smem, stream>>>(P);
+  lane_kernel<W, EPB, M><<<grid, threads, smem, stream>>>(P);
   return cudaGetLastError();
+}
+
+template <int W, int EPB>
+cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream, int* grid_out) {
+  switch (P.mode) {
+    case MODE_STEP: return launch_lanes_m<W, EPB, MODE_STEP>(P, sm_count, stream, grid_out);
+    case MODE_INIT: return launch_lanes_m<W, EPB, MODE_INIT>(P, sm_count, stream, grid_out);
+    case MODE_REFRESH:
+      return launch_lanes_m<W, EPB, MODE_REFRESH>(P, sm_count, stream, grid_out);
+    default: return launch_lanes_m<W, EPB, MODE_RESET>(P, sm_count, stream, grid_out);
+  }
 }
 
 }  // namespace tabx

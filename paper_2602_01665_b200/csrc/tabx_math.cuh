@@ -168,7 +168,11 @@ TABX_HD_CALL double libm_cos(double x) {
 struct sincos_t {
   double s, c;
 };
+#if defined(__CUDACC__) && defined(TABX_INLINE_SINCOS)
+static __host__ __device__ __forceinline__ sincos_t libm_sincos(double x) {
+#else
 TABX_HD_CALL sincos_t libm_sincos(double x) {
+#endif
   sincos_t r;
   const uint32_t k = (uint32_t)(d_to_bits(x) >> 32) & 0x7fffffffu;
   if (k >= 0x400368fdu && k < 0x419921FBu) {
