@@ -59,7 +59,18 @@ __device__ unsigned long long tabx_phase_cycles[16];
       atomicAdd(&tabx_phase_cycles[k], (unsigned long long)(ph_t1_ - ph_t0_)); \
     ph_t0_ = ph_t1_;                                                   \
   } while (0)
+// divergent regions: the lowest active lane reports
+#define TABX_PHASE_DIV(k)                                              \
+  do {                                                                 \
+    const long long ph_t1_ = clock64();                                \
+    if ((threadIdx.x & 31) == __ffs(__activemask()) - 1)               \
+      atomicAdd(&tabx_phase_cycles[k], (unsigned long long)(ph_t1_ - ph_t0_)); \
+    ph_t0_ = ph_t1_;                                                   \
+  } while (0)
 #else
+#define TABX_PHASE_DIV(k) \
+  do {                    \
+  } while (0)
 #define TABX_PHASE_BEGIN() \
   do {                     \
   } while (0)
@@ -509,6 +520,7 @@ TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* _
   // everything arrives by value (scalars in registers, the unit's vis/atk rows
   // in S.vis / S.atk): reference parameters of a non-inlined call would force
   // the caller's copies into local memory
+  TABX_PHASE_BEGIN();
   const UnitStatic U = load_static(C, i, true);
   const uint32_t* vis = &S.vis[i * W];
   const uint32_t* atk = &S.atk[i * W];
@@ -550,6 +562,7 @@ TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* _
   }
   const bool has_near = tn >= 0;
   const double tpx = S.px[tgt], tpy = S.py[tgt], tr = S.rad[tgt];
+  TABX_PHASE_DIV(14);
 
   // memory validity (heuristics.py:208-209), needed for the update either way
   const double gx = px - mx, gy = py - my;
@@ -573,6 +586,7 @@ TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* _
     const double cdev = dist > 0.0 ? lx / dist : 1.0;
     if (box && cdev >= U.cos_half) act = A_ROTATE;
   }
+  TABX_PHASE_DIV(15);
   if (act < 0 && U.ranger && has_near && sqrt(bn) < xi * U.range)
     act = best_move(px, py, S.px[tn], S.py[tn], step, true);
   if (act < 0 && has) {

@@ -28,7 +28,9 @@ PHASES = ["state load + masks", "action mask + controllers", "integrate + contac
           "team ratios, rewards, termination", "outputs + stats", "state write-back",
           "  (in controllers) mask + swamp", "  (in controllers) vis/atk cache loads",
           "  (in controllers) scripted_action", "  (in caches) zone_bits",
-          "  (in caches) publish + build_masks"]
+          "  (in caches) publish + build_masks",
+          "    (in scripted, lowest heuristic lane) statics + target loop",
+          "    (in scripted) attack / rotate-alignment check"]
 MAIN = 9
 
 
