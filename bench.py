@@ -13,9 +13,11 @@ rollout.py:360-366); auto-reset on; episodes truncate at t=400.
 * ``value``: env-steps/s of the whole job, state and outputs resident in
   HBM, CUDA-event timed over K steps (max over ranks).  Each step writes
   ~8.1 GB of observations, so every timed step streams far more than L2.
-* ``e2e``: the same metric through the trainer API (``bindings.step``)
-  with host buffers: int64 actions copied from pinned host memory every step
-  (ally team external), rewards + terminated + truncated copied back.
+* ``e2e``: the same metric through the trainer API (``bindings.HostStepper``
+  over ``bindings.step``) with host buffers: int64 actions copied from pinned
+  host memory every step (ally team external), rewards + terminated +
+  truncated copied back every step; the copies run on a copy stream and
+  overlap the neighbouring steps' kernels.
 * ``roofline``: the step kernel's algorithmic HBM bytes (SURVEY.md §8(d):
   4·N·obs_dim + 4·gdim + 4N + 7N + 3 + 8N + 2·(89N+40) per env-step) per
   launch ÷ its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
@@ -280,27 +282,33 @@ def run_gpu_arm(args) -> int:
     gen = np.random.default_rng(1234 + rank)
     pinned = [torch.from_numpy(gen.integers(0, 5, size=(per, N), dtype=np.int64)).pin_memory()
               for _ in range(4)]  # moves/rotate: always legal, no host mask round trip
-    rew_h = torch.empty((per, N), dtype=torch.float32).pin_memory()
-    term_h = torch.empty(per, dtype=torch.bool).pin_memory()
-    trunc_h = torch.empty(per, dtype=torch.bool).pin_memory()
+    # bindings.HostStepper: every step uploads its host actions and downloads
+    # its rewards / terminated / truncated through pinned double buffers on a
+    # copy stream, overlapping the neighbouring steps' kernels; the host
+    # consumes step k-1's results while step k runs
+    stepper = bindings.HostStepper(h)
+    host_sum = 0.0
 
-    def e2e_step(k):
-        a = pinned[k % len(pinned)].to(dev, non_blocking=True)
-        obs, glob, rew, term, trunc, mask = bindings.step(h, a)
-        rew_h.copy_(rew, non_blocking=True)
-        term_h.copy_(term, non_blocking=True)
-        trunc_h.copy_(trunc, non_blocking=True)
-        stream.synchronize()
+    def e2e_run(n):
+        nonlocal host_sum
+        prev = None
+        for k in range(n):
+            t = stepper.submit(pinned[k % len(pinned)])
+            if prev is not None:
+                rew_h, term_h, trunc_h = stepper.result(prev)
+                host_sum += float(rew_h[0, 0]) + int(term_h[0]) + int(trunc_h[0])
+            prev = t
+        if prev is not None:
+            rew_h, term_h, trunc_h = stepper.result(prev)
+            host_sum += float(rew_h[0, 0])
 
-    for k in range(args.warmup if e2e_steps else 0):
-        e2e_step(k)
+    e2e_run(args.warmup if e2e_steps else 0)
     barrier()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
     e0.record(stream)
-    for k in range(e2e_steps):
-        e2e_step(k)
+    e2e_run(e2e_steps)
     e1.record(stream)
     barrier()
     wall = time.perf_counter() - w0
@@ -384,8 +392,10 @@ def run_gpu_arm(args) -> int:
                        "parallelism": f"env-shard x{world}",
                        "l2": "inputs larger than L2: every step writes "
                              f"{4 * N * sim_dims(N, Z)[0] * per / 1e9:.1f} GB of observations",
-                       "e2e_workload": "bindings.step, ally external: int64 actions H2D from "
-                                       "pinned host, rewards/terminated/truncated D2H"},
+                       "e2e_workload": "bindings.HostStepper (bindings.step per step), ally "
+                                       "external: int64 actions H2D from pinned host and "
+                                       "rewards/terminated/truncated D2H every step, copies "
+                                       "overlapped with the neighbouring steps"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_env_step": bytes_per, "kernel_ms_avg": kern_avg,

@@ -278,6 +278,14 @@ int tabx_export_lanes(tabx_handle* h, const int64_t* lanes, int64_t n_lanes,
                       const tabx_state* dst);
 int tabx_import_state(tabx_handle* h, const tabx_state* src);
 
+/*
+ * Enqueue (on the handle's stream, no synchronisation) a copy of the latched
+ * first offending (env * N + unit) index of an action-mask violation
+ * (uint64, all ones = none) into dst (device or pinned host), for pipelined
+ * callers that read it back together with their step results.
+ */
+int tabx_copy_error_word(tabx_handle* h, uint64_t* dst);
+
 /* Synchronises the stream; reports (and with clear != 0 clears) the action error. */
 int tabx_get_error(tabx_handle* h, tabx_error* err, int32_t clear);
 

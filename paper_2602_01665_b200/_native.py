@@ -125,6 +125,7 @@ def lib() -> ct.CDLL:
         "tabx_export_lanes": (_i32, [P, P, ct.c_int64, ct.POINTER(TabxState)]),
         "tabx_import_state": (_i32, [P, ct.POINTER(TabxState)]),
         "tabx_get_error": (_i32, [P, ct.POINTER(TabxError), _i32]),
+        "tabx_copy_error_word": (_i32, [P, P]),
         "tabx_episode_stats": (_i32, [P, P, P, _i32]),
         "tabx_struct_sizes": (_i32, [P, P, P, P, P]),
         "tabx_reserve_configs": (_i32, [P, _i32]),

@@ -581,6 +581,14 @@ int tabx_get_error(tabx_handle* h, tabx_error* err, int32_t clear) {
   return TABX_OK;
 }
 
+int tabx_copy_error_word(tabx_handle* h, uint64_t* dst) {
+  if (!h || !dst) return fail(TABX_E_ARGUMENT, "tabx_copy_error_word: bad argument");
+  DeviceGuard guard(h->device);
+  TABX_CUDA(cudaMemcpyAsync(dst, &h->sync->err_index, 8, cudaMemcpyDefault, h->stream),
+            "error word copy");
+  return TABX_OK;
+}
+
 int tabx_episode_stats(tabx_handle* h, double* dst_host, double* dst_device, int32_t reset) {
   if (!h) return fail(TABX_E_ARGUMENT, "null handle");
   DeviceGuard guard(h->device);
