@@ -30,14 +30,14 @@ struct EmitEnv {
   uint32_t* flags;  // bit0 active, bit1 enemy
 };
 
-// Per-warp emitter scratch: the view and, for W == 1, the zone-relative
-// positions of every (observer, zone) and the visible-pair list of one chunk
-// of rows; then two stage buffers.
+// Per-warp emitter scratch: the view and, for W == 1, the env's visible
+// (observer, other) pairs in row-major order with each observer's start in
+// that list; then two stage buffers.
 template <int W>
 struct EmitScratch {
   EmitEnv<W> E;
-  float2* zq;       // [N * Z]
-  uint16_t* clist;  // [R * 32], (row-in-chunk << 5) | j
+  uint16_t* rstart;  // [N + 1]
+  uint16_t* plist;   // [N * (N - 1)], (observer << 5) | other
   float* stage;
 };
 __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -47,7 +47,7 @@ __host__ __device__ __forceinline__ size_t emit_view_bytes(int N) {
 }
 template <int W>
 __host__ __device__ __forceinline__ size_t emit_aux_bytes(int N, int Z, int R) {
-  return W == 1 ? align16((size_t)N * Z * sizeof(float2) + (size_t)R * 32 * sizeof(uint16_t)) : 0;
+  return W == 1 ? align16(((size_t)N + 1 + (size_t)N * (N - 1)) * sizeof(uint16_t)) : 0;
 }
 
 __device__ __forceinline__ bool row_bit(const uint32_t* row, int j) {
@@ -105,16 +105,21 @@ __device__ __forceinline__ void load_view(const EmitScratch<W>& X, const DevStat
     }
   }
   if constexpr (W == 1) {
-    // zone-relative positions of each active observer (perception.py:184-185)
-    if (lane < N && (E.flags[lane] & 1u)) {
-      const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
-      const double px = E.px[lane], py = E.py[lane];
-      for (int z = 0; z < Z; ++z) {
-        if (C->zone_type[z] == TABX_ZONE_NONE) continue;
-        X.zq[lane * Z + z] = make_float2(f32_quot(C->zone_cx[z] - px, fw, rw),
-                                         f32_quot(C->zone_cy[z] - py, fh, rh));
-      }
+    // visible-pair list: exclusive scan of the per-observer counts (vis
+    // already excludes inactive observers / others; drop the self bit)
+    const bool valid = lane < N;
+    uint32_t w = valid ? (E.vis[lane] & ~(1u << lane)) : 0u;
+    const int c = __popc(w);
+    int incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
     }
+    if (valid) X.rstart[lane + 1] = (uint16_t)incl;
+    if (lane == 0) X.rstart[0] = 0;
+    for (int n = incl - c; w; w &= w - 1, ++n)
+      X.plist[n] = (uint16_t)((lane << 5) | (__ffs(w) - 1));
   }
   __syncwarp();
 }
@@ -196,21 +201,28 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
   const int M = N - 1;
   const int zoff = TABX_OWN_DIM + TABX_OTHER_DIM * M;
   const int ZD = Z * TABX_ZONE_DIM;
-  // zone-block slots q = lane, lane + 32 of every active row: the template
-  // value and, for the two relative-position features of a used zone, the
-  // index into the row's zq entries (W == 1, ZD <= 64; else the generic loop)
-  const bool zfast = W == 1 && ZD <= 64;
-  float zt[2];
-  int zrel[2];
+  // Zone blocks of a chunk (W == 1, R * ZD <= 96 and R * 2Z <= 32): each lane
+  // owns up to three template slots e = lane + 32k of the chunk's zone region
+  // (row e / ZD, feature e % ZD) and one relative-position item (row, zone,
+  // axis); the decode, the template values and the zone centres are per-env
+  // registers, so a chunk costs a few stores and one quotient per lane.
+  const bool zfast = W == 1 && R * ZD <= 96 && R * 2 * Z <= 32;
+  float zt[3];
+  int zslot[3], zrow[3];
 #pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const int q = lane + 32 * t;
-    zt[t] = q < ZD ? DC->zobs[q] : 0.0f;
-    const int z = q >> 3, f = q & 7;
-    zrel[t] = (q < ZD && (f == 3 || f == 4) && C->zone_type[z] != TABX_ZONE_NONE)
-                  ? 2 * z + (f - 3)
-                  : -1;
+  for (int k = 0; k < 3; ++k) {
+    const int e = lane + 32 * k;
+    const int rr = ZD > 0 ? e / ZD : 0, q = ZD > 0 ? e - rr * ZD : 0;
+    zrow[k] = (ZD > 0 && rr < R) ? rr : -1;
+    zslot[k] = rr * D + zoff + q;
+    zt[k] = zrow[k] >= 0 ? DC->zobs[q] : 0.0f;
   }
+  const int rel_rr = Z > 0 ? lane / (2 * Z) : 0;
+  const int rel_z = Z > 0 ? (lane - rel_rr * 2 * Z) >> 1 : 0, rel_ax = lane & 1;
+  const bool rel_on = Z > 0 && rel_rr < R && C->zone_type[rel_z] != TABX_ZONE_NONE;
+  const double rel_c = rel_on ? (rel_ax ? C->zone_cy[rel_z] : C->zone_cx[rel_z]) : 0.0;
+  const double rel_f = rel_ax ? fh : fw, rel_rf = rel_ax ? rh : rw;
+  const int rel_off = rel_rr * D + zoff + rel_z * TABX_ZONE_DIM + 3 + rel_ax;
   if (obs) {
     for (int r0 = 0; r0 < N; r0 += R) {
       const int nr = min(R, N - r0);
@@ -259,19 +271,10 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
         blk[16] = row_bit(&E.atk[r * W], j) ? 1.0f : 0.0f;
       };
       if constexpr (W == 1) {
-        // compact the chunk's visible pairs (row-major) with ballots
-        int cnt = 0;
-        const uint32_t lt = (1u << lane) - 1u;
-        for (int rr = 0; rr < nr; ++rr) {
-          const int r = r0 + rr;
-          const uint32_t w = E.vis[r] & ~(1u << r);
-          if ((w >> lane) & 1u) X.clist[cnt + __popc(w & lt)] = (uint16_t)((rr << 5) | lane);
-          cnt += __popc(w);
-        }
-        __syncwarp();
-        for (int p = lane; p < cnt; p += 32) {
-          const int rj = X.clist[p];
-          pair_block(r0 + (rj >> 5), rj & 31);
+        const int p1 = X.rstart[r0 + nr];
+        for (int p = X.rstart[r0] + lane; p < p1; p += 32) {
+          const int rj = X.plist[p];
+          pair_block(rj >> 5, rj & 31);
         }
       } else {
         int total = 0;
@@ -301,32 +304,29 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
       }
       // zone blocks of the active rows: the config's template with the
       // observer-relative position (unused zone slots stay zero)
-      for (int rr = 0; rr < nr; ++rr) {
-        const int r = r0 + rr;
-        if (!(E.flags[r] & 1u)) continue;
-        float* zb = row0 + rr * D + zoff;
-        if (zfast) {
-          const float* zr = reinterpret_cast<const float*>(X.zq) + 2 * r * Z;
+      if (zfast) {
 #pragma unroll
-          for (int t = 0; t < 2; ++t)
-            if (lane + 32 * t < ZD) zb[lane + 32 * t] = zrel[t] >= 0 ? zr[zrel[t]] : zt[t];
-          continue;
+        for (int k = 0; k < 3; ++k)
+          if (zrow[k] >= 0 && zrow[k] < nr && (E.flags[r0 + zrow[k]] & 1u)) row0[zslot[k]] = zt[k];
+        __syncwarp();  // the relative positions overwrite template slots
+        if (rel_on && rel_rr < nr) {
+          const int r = r0 + rel_rr;
+          if (E.flags[r] & 1u)
+            row0[rel_off] = f32_quot(rel_c - (rel_ax ? E.py[r] : E.px[r]), rel_f, rel_rf);
         }
-        for (int q = lane; q < ZD; q += 32) {
-          const int z = q >> 3, f = q & 7;
-          float v = DC->zobs[q];
-          if (f == 3 || f == 4) {
-            if (C->zone_type[z] != TABX_ZONE_NONE) {
-              if constexpr (W == 1) {
-                const float2 zr = X.zq[r * Z + z];
-                v = f == 3 ? zr.x : zr.y;
-              } else {
-                v = f == 3 ? f32_quot(C->zone_cx[z] - E.px[r], fw, rw)
-                           : f32_quot(C->zone_cy[z] - E.py[r], fh, rh);
-              }
-            }
+      } else {
+        for (int rr = 0; rr < nr; ++rr) {
+          const int r = r0 + rr;
+          if (!(E.flags[r] & 1u)) continue;
+          float* zb = row0 + rr * D + zoff;
+          for (int q = lane; q < ZD; q += 32) {
+            const int z = q >> 3, f = q & 7;
+            float v = DC->zobs[q];
+            if ((f == 3 || f == 4) && C->zone_type[z] != TABX_ZONE_NONE)
+              v = f == 3 ? f32_quot(C->zone_cx[z] - E.px[r], fw, rw)
+                         : f32_quot(C->zone_cy[z] - E.py[r], fh, rh);
+            zb[q] = v;
           }
-          zb[q] = v;
         }
       }
       fence_proxy_async();
@@ -397,8 +397,8 @@ __device__ __forceinline__ EmitScratch<W> emit_scratch(unsigned char* base, int 
   X.E.atk = X.E.vis + N * W;
   X.E.flags = X.E.atk + N * W;
   p += align16((size_t)4 * N * (2 * W + 1));
-  X.zq = reinterpret_cast<float2*>(p);
-  X.clist = reinterpret_cast<uint16_t*>(p + (size_t)N * Z * sizeof(float2));
+  X.rstart = reinterpret_cast<uint16_t*>(p);
+  X.plist = X.rstart + N + 1;
   X.stage = reinterpret_cast<float*>(p + emit_aux_bytes<W>(N, Z, R));
   return X;
 }
