@@ -208,14 +208,14 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
   // registers, so a chunk costs a few stores and one quotient per lane.
   const bool zfast = W == 1 && R * ZD <= 96 && R * 2 * Z <= 32;
   float zt[3];
-  int zslot[3], zrow[3];
+  int zinfo[3];  // (row + 1) << 16 | offset in the chunk; 0 = no slot
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const int e = lane + 32 * k;
     const int rr = ZD > 0 ? e / ZD : 0, q = ZD > 0 ? e - rr * ZD : 0;
-    zrow[k] = (ZD > 0 && rr < R) ? rr : -1;
-    zslot[k] = rr * D + zoff + q;
-    zt[k] = zrow[k] >= 0 ? DC->zobs[q] : 0.0f;
+    const bool on = ZD > 0 && rr < R;
+    zinfo[k] = on ? ((rr + 1) << 16) | (rr * D + zoff + q) : 0;
+    zt[k] = on ? DC->zobs[q] : 0.0f;
   }
   const int rel_rr = Z > 0 ? lane / (2 * Z) : 0;
   const int rel_z = Z > 0 ? (lane - rel_rr * 2 * Z) >> 1 : 0, rel_ax = lane & 1;
@@ -307,7 +307,10 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
       if (zfast) {
 #pragma unroll
         for (int k = 0; k < 3; ++k)
-          if (zrow[k] >= 0 && zrow[k] < nr && (E.flags[r0 + zrow[k]] & 1u)) row0[zslot[k]] = zt[k];
+        {
+          const int rr = (zinfo[k] >> 16) - 1;
+          if (rr >= 0 && rr < nr && (E.flags[r0 + rr] & 1u)) row0[zinfo[k] & 0xFFFF] = zt[k];
+        }
         __syncwarp();  // the relative positions overwrite template slots
         if (rel_on && rel_rr < nr) {
           const int r = r0 + rel_rr;
