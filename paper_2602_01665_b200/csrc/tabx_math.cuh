@@ -163,8 +163,32 @@ TABX_HD_CALL double libm_cos(double x) {
   return cos(x);
 }
 
-// (sin x, cos x) with the large-argument reduction shared; each component is
-// exactly libm_sin(x) / libm_cos(x).
+// do_sin with its small-argument Taylor branch evaluated alongside the table
+// path and selected, so lanes of a warp never diverge on it.
+TABX_HD double libm_do_sin_sel(double x, double dx) {
+  typedef libm_consts K;
+  const double tay = taylor_sin(x * x, x, dx);
+  const double ax = fabs(x);
+  const double d = x <= 0 ? -dx : dx;
+  const double u = TABX_BIG + ax;
+  const double xr = ax - (u - TABX_BIG);
+  const double xx = xr * xr;
+  const double s = xr + fma(xr * xx, fma(xx, K::sn5, K::sn3), d);
+  const double c = fma(xr, d, xx * fma(fma(xx, K::cs6, K::cs4), xx, K::cs2));
+  const double* e = sc_entry(u);
+  const double cor = fma(e[2], s, fma(-e[0], c, fma(s, e[3], e[1])));
+  const double tab = copysign(e[0] + cor, x);
+  return ax < 0.126 ? tay : tab;
+}
+
+// (sin x, cos x), each component exactly libm_sin(x) / libm_cos(x), with
+// warp-uniform control flow: glibc picks, by |x|, the arguments of one
+// do_sin and one do_cos evaluation (|x| < 0.855: (x, 0) for both; < 2.426:
+// cos-of-complement arguments; else the Cody-Waite reduction, quadrant n)
+// and how their results map to sin and cos.  Here every lane computes the
+// three argument sets, selects its own, runs do_sin and do_cos once, and
+// selects the outputs -- the same float64 operations per lane as the
+// branchy reference, without serialising a warp over its lanes' ranges.
 struct sincos_t {
   double s, c;
 };
@@ -175,15 +199,35 @@ TABX_HD_CALL sincos_t libm_sincos(double x) {
 #endif
   sincos_t r;
   const uint32_t k = (uint32_t)(d_to_bits(x) >> 32) & 0x7fffffffu;
-  if (k >= 0x400368fdu && k < 0x419921FBu) {
-    double a, da;
-    const int n = libm_reduce(x, &a, &da);
-    r.s = libm_do_sincos(a, da, n);
-    r.c = libm_do_sincos(a, da, n + 1);
-  } else {
+  if (k >= 0x419921FBu) {  // outside the restated range (never a heading)
     r.s = libm_sin(x);
     r.c = libm_cos(x);
+    return r;
   }
+  const bool r1 = k < 0x3feb6000u, r2 = !r1 && k < 0x400368fdu;
+  double a3, da3;
+  const int n = libm_reduce(x, &a3, &da3);
+  const double y = TABX_HP0 - fabs(x);
+  const double a2 = y + TABX_HP1;
+  const double da2 = (y - a2) + TABX_HP1;
+  const double sa = r1 ? x : (r2 ? a2 : a3), sda = r1 ? 0.0 : (r2 ? da2 : da3);
+  const double ca = r1 ? x : (r2 ? y : a3), cda = r1 ? 0.0 : (r2 ? TABX_HP1 : da3);
+  const double vs = libm_do_sin_sel(sa, sda);
+  const double vc = libm_do_cos(ca, cda);
+  if (r1) {
+    r.s = vs;
+    r.c = vc;
+  } else if (r2) {
+    r.s = copysign(vc, x);
+    r.c = vs;
+  } else {
+    const double s0 = (n & 1) ? vc : vs;
+    const double c0 = ((n + 1) & 1) ? vc : vs;
+    r.s = (n & 2) ? -s0 : s0;
+    r.c = ((n + 1) & 2) ? -c0 : c0;
+  }
+  if (k < 0x3e500000u) r.s = x;
+  if (k < 0x3e400000u) r.c = 1.0;
   return r;
 }
 
