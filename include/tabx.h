@@ -342,6 +342,27 @@ int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state, int64_t
                       int64_t* pcg64);
 
 /*
+ * Policy helper of the on-device rollout loop (C5): for each of m agents,
+ * Gumbel-max sample over the legal actions (mask row of 7 bytes) of its
+ * logits (float32, or bfloat16 with logits_bf16 != 0; row stride ld >= 7
+ * elements) and the sampled action's log-probability under the masked
+ * softmax.  Noise = counter hash of (seed, *step_ptr + step_add, agent,
+ * action); step_ptr (device, may be NULL) lets a replayed CUDA graph draw
+ * fresh noise.  Asynchronous on `stream`.
+ */
+int tabx_masked_sample(const void* logits, int32_t logits_bf16, int64_t ld,
+                       const uint8_t* mask, int64_t m, uint64_t seed, const uint64_t* step_ptr,
+                       uint64_t step_add, int64_t* actions, float* logp, void* stream);
+
+/*
+ * Policy input of the rollout loop: float32 rows [rows, d] (observations) ->
+ * bfloat16 rows [rows, dp], dp a multiple of 8, zero padded (16-byte aligned
+ * GEMM operand).  Asynchronous on `stream`.
+ */
+int tabx_pack_bf16(const float* src, int64_t rows, int32_t d, int32_t dp, void* dst,
+                   void* stream);
+
+/*
  * Tool hook: SM cycles per step phase summed over envs (W = 1 step kernel),
  * nonzero only in a build with -DTABX_PHASE_PROF (tools/phase_prof.py).
  */

@@ -28,6 +28,12 @@ cudaError_t launch_spawn_lanes(const DevState& st, const tabx_config* cfgs,
                                const uint64_t* seeds, int64_t n, int N, int W, int sm_count,
                                cudaStream_t stream);
 cudaError_t phase_cycles_w1(unsigned long long* host16, int reset);
+cudaError_t launch_masked_sample(const void* logits, int bf16, int64_t ld, const uint8_t* mask,
+                                 int64_t M, uint64_t seed, const uint64_t* step_ptr,
+                                 uint64_t step_add, int64_t* actions, float* logp, int sm_count,
+                                 cudaStream_t stream);
+cudaError_t launch_pack_bf16(const float* src, int64_t rows, int D, int Dp, void* dst,
+                             int sm_count, cudaStream_t stream);
 cudaError_t launch_export(const DevState& st, const tabx_state& d, const int64_t* lanes,
                           int64_t rows, int N, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_import(const DevState& st, const tabx_state& s, const tabx_config* cfgs,
@@ -637,6 +643,36 @@ int tabx_struct_sizes(int64_t* config, int64_t* outputs, int64_t* state, int64_t
   if (state) *state = (int64_t)sizeof(tabx_state);
   if (level_spec) *level_spec = (int64_t)sizeof(tabx_level_spec);
   if (pcg64) *pcg64 = (int64_t)sizeof(tabx_pcg64);
+  return TABX_OK;
+}
+
+int tabx_masked_sample(const void* logits, int32_t logits_bf16, int64_t ld,
+                       const uint8_t* mask, int64_t m, uint64_t seed, const uint64_t* step_ptr,
+                       uint64_t step_add, int64_t* actions, float* logp, void* stream) {
+  if (m < 0 || (m > 0 && (!logits || !mask || !actions || !logp)) || ld < TABX_NUM_ACTIONS)
+    return fail(TABX_E_ARGUMENT, "tabx_masked_sample: bad argument");
+  static int sm_count = 0;
+  if (!sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sm_count = 148;
+  }
+  TABX_CUDA(launch_masked_sample(logits, logits_bf16, ld, mask, m, seed, step_ptr, step_add,
+                                 actions, logp, sm_count, (cudaStream_t)stream),
+            "masked sample");
+  return TABX_OK;
+}
+
+int tabx_pack_bf16(const float* src, int64_t rows, int32_t d, int32_t dp, void* dst,
+                   void* stream) {
+  if (rows < 0 || d < 1 || dp < d || (dp & 7) || (rows > 0 && (!src || !dst)) ||
+      ((uintptr_t)dst & 15))
+    return fail(TABX_E_ARGUMENT, "tabx_pack_bf16: bad argument");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  TABX_CUDA(launch_pack_bf16(src, rows, d, dp, dst, sms, (cudaStream_t)stream), "pack bf16");
   return TABX_OK;
 }
 

@@ -9,8 +9,13 @@ once into a CUDA graph and replayed per iteration.
 
 Policies: ``random`` (uniform over legal actions, the reference's random
 controller semantics) or ``mlp`` (a bf16 two-layer MLP over the per-agent
-observation, masked Gumbel-max sampling).  The ally team is driven by the
-policy (external controller); the enemy keeps its scenario controller.
+observation).  Either way the actions come from the library's fused masked
+Gumbel-max sampler (``tabx_masked_sample``: one pass per agent producing the
+action and its log-probability, noise keyed on a device step counter so the
+replayed graph draws fresh noise).  The MLP reads a bf16 copy of the
+observation padded to a multiple of 8 features (aligned GEMM rows) and emits
+8 logits of which the first 7 are the actions.  The ally team is driven by
+the policy (external controller); the enemy keeps its scenario controller.
 """
 from __future__ import annotations
 
@@ -26,10 +31,13 @@ from .sim import BatchSim
 
 
 class MLPPolicy(torch.nn.Module):
+    """Two-layer MLP over padded per-agent observations -> 8 logits (7 used)."""
+
     def __init__(self, obs_dim: int, hidden: int = 128, n_actions: int = 7):
         super().__init__()
-        self.l1 = torch.nn.Linear(obs_dim, hidden)
-        self.l2 = torch.nn.Linear(hidden, n_actions)
+        self.in_dim = (obs_dim + 7) // 8 * 8
+        self.l1 = torch.nn.Linear(self.in_dim, hidden)
+        self.l2 = torch.nn.Linear(hidden, (n_actions + 7) // 8 * 8)
 
     def forward(self, obs: torch.Tensor) -> torch.Tensor:
         h = torch.relu(self.l1(obs))
@@ -37,7 +45,8 @@ class MLPPolicy(torch.nn.Module):
 
 
 def masked_sample(logits: torch.Tensor, mask: torch.Tensor):
-    """Gumbel-max sample over legal actions; returns (actions int64, logp f32)."""
+    """Gumbel-max sample over legal actions with torch ops (reference
+    semantics of the fused sampler); returns (actions int64, logp f32)."""
     u = torch.rand_like(logits, dtype=torch.float32).clamp_(1e-12, 1.0)
     g = -torch.log(-torch.log(u))
     neg = torch.finfo(torch.float32).min
@@ -81,8 +90,13 @@ class Rollout:
         self.policy = None
         if policy == "mlp":
             self.policy = MLPPolicy(D, hidden).to(dev).to(torch.bfloat16)
-        elif policy != "random":
+            self._xin = torch.zeros(B, N, self.policy.in_dim, dtype=torch.bfloat16, device=dev)
+        elif policy == "random":
+            self._zero_logits = torch.zeros(B * N, 8, device=dev)
+        else:
             raise ValueError(f"unknown policy {policy!r}")
+        self.seed = int(seed)
+        self._ctr = torch.zeros(1, dtype=torch.int64, device=dev)  # sampler noise counter
         self._outs = []
         for t in range(T):
             o = nat.TabxOutputs()
@@ -111,20 +125,27 @@ class Rollout:
     def _step(self, t):
         mask = self.sim._buf["action_mask"]
         obs = self._current_obs(t)
-        if self.policy is None:
-            logits = torch.zeros(self.B, self.N, 7, device=self.device)
-        else:
-            logits = self.policy(obs.to(torch.bfloat16))
-        act, logp = masked_sample(logits, mask)
-        self.buf.actions[t].copy_(act)
-        self.buf.logp[t].copy_(logp)
         L = nat.lib()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        if self.policy is None:
+            logits, bf16 = self._zero_logits, 0
+        else:
+            nat.check(L.tabx_pack_bf16(ct.c_void_p(obs.data_ptr()), self.B * self.N, self.D,
+                                       self.policy.in_dim, ct.c_void_p(self._xin.data_ptr()),
+                                       ct.c_void_p(stream)), "tabx_pack_bf16")
+            logits, bf16 = self.policy(self._xin).reshape(self.B * self.N, -1), 1
+        nat.check(L.tabx_masked_sample(
+            ct.c_void_p(logits.data_ptr()), bf16, logits.shape[-1], ct.c_void_p(mask.data_ptr()),
+            self.B * self.N, ct.c_uint64(self.seed), ct.c_void_p(self._ctr.data_ptr()), t,
+            ct.c_void_p(self.buf.actions[t].data_ptr()), ct.c_void_p(self.buf.logp[t].data_ptr()),
+            ct.c_void_p(stream)), "tabx_masked_sample")
         nat.check(L.tabx_step(self.sim.handle, ct.c_void_p(self.buf.actions[t].data_ptr()),
                               ct.byref(self._outs[t])), "tabx_step")
 
     def _horizon(self):
         for t in range(self.T):
             self._step(t)
+        self._ctr.add_(self.T)  # next horizon's noise
 
     def _set_stream(self, stream):
         nat.check(nat.lib().tabx_set_stream(self.sim.handle, ct.c_void_p(stream.cuda_stream)),

@@ -1,0 +1,63 @@
+"""Fused masked sampler of the C5 rollout loop (``tabx_masked_sample``).
+
+Every sampled action is legal, its log-probability equals the masked
+log-softmax of the logits at that action, equal logits give the uniform
+distribution over the legal set (the reference's random controller,
+environment.py:198-201, up to the RNG stream), and peaked logits pick their
+argmax.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+
+import pytest
+import torch
+
+from paper_2602_01665_b200 import _native as nat
+
+pytestmark = pytest.mark.gpu
+
+
+def sample(logits, mask, seed=1, step=0, bf16=False):
+    M = mask.shape[0]
+    act = torch.empty(M, dtype=torch.int64, device=mask.device)
+    logp = torch.empty(M, dtype=torch.float32, device=mask.device)
+    lg = logits.to(torch.bfloat16 if bf16 else torch.float32).contiguous()
+    nat.check(nat.lib().tabx_masked_sample(
+        ct.c_void_p(lg.data_ptr()), int(bf16), lg.shape[1], ct.c_void_p(mask.data_ptr()), M,
+        ct.c_uint64(seed), None, step, ct.c_void_p(act.data_ptr()), ct.c_void_p(logp.data_ptr()),
+        ct.c_void_p(torch.cuda.current_stream().cuda_stream)), "tabx_masked_sample")
+    torch.cuda.synchronize()
+    return act, logp
+
+
+@pytest.mark.parametrize("bf16", [False, True])
+def test_legal_and_logp(bf16):
+    g = torch.Generator(device="cuda").manual_seed(0)
+    M = 200_000
+    mask = torch.rand(M, 7, device="cuda", generator=g) < 0.6
+    mask[:, 6] |= ~mask.any(1)  # at least one legal action per row
+    logits = torch.randn(M, 8, device="cuda", generator=g)
+    act, logp = sample(logits, mask.to(torch.uint8), bf16=bf16)
+    assert bool(torch.gather(mask, 1, act[:, None]).all())
+    lg = logits[:, :7].to(torch.bfloat16 if bf16 else torch.float32).float()
+    ref = torch.log_softmax(torch.where(mask, lg, torch.tensor(float("-inf"), device="cuda")), 1)
+    want = torch.gather(ref, 1, act[:, None])[:, 0]
+    assert torch.allclose(logp, want, atol=2e-5, rtol=1e-5)
+
+
+def test_uniform_and_argmax():
+    M = 400_000
+    mask = torch.zeros(M, 7, dtype=torch.uint8, device="cuda")
+    mask[:, [0, 2, 5]] = 1
+    act, _ = sample(torch.zeros(M, 8, device="cuda"), mask, seed=7, step=3)
+    counts = torch.bincount(act, minlength=7).float() / M
+    assert set(torch.nonzero(counts).flatten().tolist()) == {0, 2, 5}
+    assert torch.allclose(counts[[0, 2, 5]], torch.full((3,), 1 / 3, device="cuda"), atol=5e-3)
+    peaked = torch.zeros(M, 8, device="cuda")
+    peaked[:, 2] = 40.0
+    act, logp = sample(peaked, mask, seed=7, step=4)
+    assert bool((act == 2).all()) and float(logp.abs().max()) < 1e-6
+    a1, _ = sample(torch.zeros(M, 8, device="cuda"), mask, seed=7, step=5)
+    a2, _ = sample(torch.zeros(M, 8, device="cuda"), mask, seed=7, step=6)
+    assert not torch.equal(a1, a2)  # the step counter changes the noise
