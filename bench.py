@@ -5,8 +5,9 @@
     python bench.py --impl reference ...     # the reference's CPU step (oracle port)
 
 Workload (BASELINE.json configs[2], the metric's config): C3 = 10v10
-heterogeneous roles on the 2L2B2S terrain map, 262,144 environments in total,
-sharded over the ranks (strong scaling).  Ally team on the in-engine random
+heterogeneous roles on the 2L2B2S terrain map, 262,144 environments per GPU
+(weak scaling: rank g owns global lanes [g*B, (g+1)*B) with their global lane
+seeds; no per-step communication).  Ally team on the in-engine random
 controller, enemy heuristic-medium (the reference bench's ``_scripted`` rule,
 rollout.py:360-366); auto-reset on; episodes truncate at t=400.
 
@@ -193,7 +194,7 @@ def run_reference_arm(args) -> int:
     line = {
         "metric": "env_steps_per_s", "value": v, "unit": "env-steps/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * r["seconds"] / r["steps"],
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (scenario JSON, seeded lanes)", "impl": "reference",
         "agent_steps_per_s": v * sc_units,
         "config": {"workload": WORKLOAD[args.scenario], "scenario": SCENARIOS[args.scenario],
@@ -224,8 +225,11 @@ def run_gpu_arm(args) -> int:
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    total = args.envs or DEFAULT_ENVS[args.scenario]
-    first, per = shard.shard_range(total, world, rank)
+    # weak scaling: every GPU steps its own full batch (lanes are independent;
+    # rank g owns the global lanes [g*per, (g+1)*per) with their global seeds)
+    per = args.envs or DEFAULT_ENVS[args.scenario]
+    total = per * world
+    first, _ = shard.shard_range(total, world, rank)
     base = builtin_scenario(SCENARIOS[args.scenario])
     sc = base.scripted()
     N, Z = sc.max_units, sc.max_zones
@@ -383,7 +387,7 @@ def run_gpu_arm(args) -> int:
         line = {
             "metric": "env_steps_per_s", "value": value, "unit": "env-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (scenario JSON, seeded lanes)",
             "agent_steps_per_s": value * len(sc.units),
             "config": {"workload": WORKLOAD[args.scenario], "scenario": SCENARIOS[args.scenario],
@@ -432,7 +436,8 @@ def main(argv=None) -> int:
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("tabx", "reference"), default="tabx")
     ap.add_argument("--scenario", choices=sorted(SCENARIOS), default="c3")
-    ap.add_argument("--envs", type=int, default=0, help="total environments (all ranks)")
+    ap.add_argument("--envs", type=int, default=0,
+                    help="environments per GPU (weak scaling: the job runs n_gpus x envs)")
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-envs", type=int, default=1024)
