@@ -312,3 +312,66 @@ def test_graph_rollout_replays_exactly(policy):
         assert torch.equal(out.terminated, buf.terminated[t]), t
         mask = out.action_mask.clone()
     ro.close()
+
+
+def _many_zones(n_zones: int):
+    """duel_terrain with n_zones overlapping zones (lava stacks at the centre,
+    so the burn is a numpy pairwise sum once Z >= 8; bushes and swamps around)."""
+    import dataclasses
+
+    from paper_2602_01665_b200.scenario import Zone
+    base = builtin_scenario("duel_terrain")
+    kinds = ("lava", "bush", "swamp")
+    zones = []
+    for k in range(n_zones):
+        t = kinds[k % 3]
+        if t == "lava":
+            zones.append(Zone("lava", (20.0 + 0.3 * (k % 5), 20.0), (6.0 + k * 0.7, 4.0 + k * 0.3),
+                              1.5 + 0.37 * k))
+        elif t == "bush":
+            zones.append(Zone("bush", (8.0 + 2.5 * (k % 9), 12.0 + (k % 4)), (3.0, 2.0), 0.0))
+        else:
+            zones.append(Zone("swamp", (30.0 - (k % 7), 28.0), (4.0, 3.0 + 0.1 * k),
+                              0.3 + 0.02 * k))
+    return dataclasses.replace(base, zones=zones, max_zones=n_zones, notes=list(base.notes))
+
+
+@pytest.mark.parametrize("n_zones,B,seed", [(12, 128, 7), (24, 64, 8), (32, 32, 9)])
+def test_many_zones_match_oracle(n_zones, B, seed):
+    """Zone counts beyond the benchmark maps: the pairwise lava sum (Z >= 8),
+    the generic zone-block path of the observation kernel, wide zone masks."""
+    sc = _many_zones(n_zones).with_controllers(ally="random", enemy="heuristic:medium")
+    ora = _perturbed_states(sc, B, seed)
+    ora.sim.pos[:, :, :] = np.clip(ora.sim.pos, 0.0, 40.0) * 0.5 + 10.0  # pull into the zones
+    orc.fresh_caches(ora.sim)
+    gpu = BatchSim([sc] * B, ora.sim.seed.copy(), auto_reset=True, device="cuda:0")
+    gpu.import_state(oracle_state_dict(ora.sim))
+    for t in range(4):
+        o = ora.step(None)
+        g = gpu.step(None)
+        bad = compare_outputs(g, o, f"Z={n_zones} step {t}")
+        bad += compare_state(gpu.export_state(), ora.sim, f"Z={n_zones} step {t}")
+        assert not bad, "\n".join(bad[:10])
+
+
+def test_two_word_rows_with_zones_match_oracle():
+    """W = 2 (40 units) on a map with 10 zones: the multi-word visibility rows,
+    the per-CTA env layout and the generic zone / pair paths of the
+    observation kernel."""
+    import dataclasses
+    base = builtin_scenario("c4_50v50")
+    allies = [u for u in base.units if u.team == 0][:20]
+    enemies = [u for u in base.units if u.team == 1][:20]
+    zones = _many_zones(10).zones
+    sc = dataclasses.replace(base, units=allies + enemies, zones=zones, max_units=40,
+                             max_zones=10, notes=list(base.notes))
+    sc = sc.with_controllers(ally="random", enemy="heuristic:medium")
+    ora = _perturbed_states(sc, 24, 10)
+    gpu = BatchSim([sc] * 24, ora.sim.seed.copy(), auto_reset=True, device="cuda:0")
+    gpu.import_state(oracle_state_dict(ora.sim))
+    for t in range(3):
+        o = ora.step(None)
+        g = gpu.step(None)
+        bad = compare_outputs(g, o, f"W=2 step {t}")
+        bad += compare_state(gpu.export_state(), ora.sim, f"W=2 step {t}")
+        assert not bad, "\n".join(bad[:10])
