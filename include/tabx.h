@@ -363,7 +363,7 @@ int tabx_pack_bf16(const float* src, int64_t rows, int32_t d, int32_t dp, void* 
                    void* stream);
 
 /*
- * Tool hook: SM cycles per step phase summed over envs (W = 1 step kernel),
+ * Tool hook: SM cycles per step phase summed over envs (all step kernels),
  * nonzero only in a build with -DTABX_PHASE_PROF (tools/phase_prof.py).
  */
 int tabx_debug_phase_cycles(uint64_t* host16, int32_t reset);

@@ -28,6 +28,9 @@ cudaError_t launch_spawn_lanes(const DevState& st, const tabx_config* cfgs,
                                const uint64_t* seeds, int64_t n, int N, int W, int sm_count,
                                cudaStream_t stream);
 cudaError_t phase_cycles_w1(unsigned long long* host16, int reset);
+cudaError_t phase_cycles_w2(unsigned long long* host16, int reset);
+cudaError_t phase_cycles_w4(unsigned long long* host16, int reset);
+cudaError_t phase_cycles_w8(unsigned long long* host16, int reset);
 cudaError_t launch_masked_sample(const void* logits, int bf16, int64_t ld, const uint8_t* mask,
                                  int64_t M, uint64_t seed, const uint64_t* step_ptr,
                                  uint64_t step_add, int64_t* actions, float* logp, int sm_count,
@@ -678,7 +681,14 @@ int tabx_pack_bf16(const float* src, int64_t rows, int32_t d, int32_t dp, void* 
 
 int tabx_debug_phase_cycles(uint64_t* host16, int32_t reset) {
   if (!host16) return fail(TABX_E_ARGUMENT, "tabx_debug_phase_cycles: bad argument");
-  TABX_CUDA(phase_cycles_w1((unsigned long long*)host16, reset), "phase cycles");
+  unsigned long long part[16];
+  for (int k = 0; k < 16; ++k) host16[k] = 0;
+  cudaError_t (*fns[4])(unsigned long long*, int) = {phase_cycles_w1, phase_cycles_w2,
+                                                      phase_cycles_w4, phase_cycles_w8};
+  for (auto fn : fns) {
+    TABX_CUDA(fn(part, reset), "phase cycles");
+    for (int k = 0; k < 16; ++k) host16[k] += part[k];
+  }
   return TABX_OK;
 }
 

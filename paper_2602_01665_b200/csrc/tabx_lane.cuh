@@ -956,6 +956,9 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   // float32 filter on squared distance vs rs^2 (margin 1e-5 relative);
   // near-contact pairs get the reference's float64 depth test
   bool any_touch = false;
+  uint32_t rowm[W];  // W > 1: rows (observers a) with a touching pair (a, c > a)
+#pragma unroll
+  for (int k = 0; k < W; ++k) rowm[k] = 0u;
   if (W == 1) {
     // all 32 lanes over the N(N-1)/2 pairs; one ballot word per 32 pairs keeps
     // the ascending (i, j) order the Gauss-Seidel solve needs
@@ -1022,7 +1025,9 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     }
 #pragma unroll
     for (int k = 0; k < W; ++k) S.touch[i * W + k] = trow[k];
-    any_touch = env_any<W>(mine, S, i);
+    env_ballot<W>(mine, S, i, rowm);
+#pragma unroll
+    for (int k = 0; k < W; ++k) any_touch |= rowm[k] != 0u;
   }
   double vfx = vux, vfy = vuy;
   if (any_touch) {
@@ -1034,7 +1039,10 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     if (i == 0) {
       const double e = C->restitution, slop = C->slop, beta = C->correction;
       const int NP = N * (N - 1) / 2;
-      for (int a0 = 0; a0 < (W == 1 ? 1 : N); ++a0) {
+      // rows in ascending order (W > 1: only those with a touching pair)
+      for (int kk = 0; kk < (W == 1 ? 1 : W); ++kk)
+      for (uint32_t rows = W == 1 ? 1u : rowm[kk]; rows; rows &= rows - 1) {
+        const int a0 = W == 1 ? 0 : (kk << 5) + __ffs(rows) - 1;
         for (int k = 0; k < (W == 1 ? (NP + 31) >> 5 : W); ++k) {
           uint32_t m = W == 1 ? S.tmask[k] : S.touch[a0 * W + k];
           while (m) {

@@ -8,4 +8,19 @@ cudaError_t launch_lanes_w2(const Params& P, int sm_count, cudaStream_t stream, 
 cudaError_t launch_emit_w2(const Params& P, int sm_count, cudaStream_t stream) {
   return launch_emit_t<2, 4>(P, sm_count, stream);
 }
+// Phase cycle counters of the instrumented build (zeros otherwise).
+cudaError_t phase_cycles_w2(unsigned long long* host16, int reset) {
+#ifdef TABX_PHASE_PROF
+  cudaError_t e = cudaMemcpyFromSymbol(host16, tabx_phase_cycles, 16 * sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    static const unsigned long long zero[16] = {};
+    e = cudaMemcpyToSymbol(tabx_phase_cycles, zero, sizeof(zero));
+  }
+  return e;
+#else
+  (void)reset;
+  for (int k = 0; k < 16; ++k) host16[k] = 0;
+  return cudaSuccess;
+#endif
+}
 }  // namespace tabx
