@@ -523,7 +523,7 @@ constexpr int SA_ACT_MASK = 0xff, SA_HAS = 0x100, SA_MEMOK = 0x200, SA_TGT_SHIFT
 template <int W>
 TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
                                int N, int Z, double hd, double cd, double step,
-                               uint32_t mask7, double u_explore, uint64_t seed, uint64_t t_step,
+                               uint32_t mask7, double u_explore, double u_pick,
                                double eps, double xi, uint32_t bush_m, double mx, double my,
                                bool memv) {
   // everything arrives by value (scalars in registers, the unit's vis/atk rows
@@ -627,8 +627,9 @@ TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* _
     act = best_move(px, py, C->zone_cx[nb], C->zone_cy[nb], step, false);
   }
   if (act < 0) act = A_ROTATE;
-  // epsilon exploration; the pick draw is only needed when exploring
-  if (u_explore < eps) act = kth_legal(mask7, uniform53(seed, t_step, TAG_PICK, (uint64_t)i));
+  // epsilon exploration (the pick draw is made by the caller, beside the
+  // explore draw: two independent hash chains interleave)
+  if (u_explore < eps) act = kth_legal(mask7, u_pick);
   // packed result: action, memory update (has -> remember tgt; memv = has || mem_ok)
   return act | (has ? SA_HAS : 0) | (mem_ok ? SA_MEMOK : 0) | (tgt << SA_TGT_SHIFT);
 }
@@ -913,10 +914,11 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
         }
       }
       const double ue = uniform53(seed, (uint64_t)(int64_t)t, TAG_EXPLORE, (uint64_t)i);
+      const double up = uniform53(seed, (uint64_t)(int64_t)t, TAG_PICK, (uint64_t)i);
       const double stepl = speff * dt;
-      const int r = scripted_action<W>(S, C, i, N, Z, hd, cd, stepl, mask7, ue, seed,
-                                       (uint64_t)(int64_t)t, C->epsilon[team],
-                                       C->aggressive[team], bush_m, mx, my, memv);
+      const int r = scripted_action<W>(S, C, i, N, Z, hd, cd, stepl, mask7, ue, up,
+                                       C->epsilon[team], C->aggressive[team], bush_m, mx, my,
+                                       memv);
       act = r & SA_ACT_MASK;
       if (r & SA_HAS) {
         const int tg = r >> SA_TGT_SHIFT;
