@@ -367,7 +367,7 @@ def run_gpu_arm(args) -> int:
         obs_bytes = 4 * N * D + 4 * G + 57 * N + 5  # writes + the per-unit view it reads
         step_bytes = bytes_per - (4 * N * D + 4 * G)
         kernels = []
-        for name, ms, nbytes in (("step_kernel (K1: actions..rewards, caches, state)",
+        for name, ms, nbytes in (("step_kernels (K0 heuristic-controller pass + K1 actions..rewards, caches, state)",
                                   kprof["step_kernel_ms"], step_bytes),
                                  ("obs_kernel (K2: observation + global-state stream, TMA)",
                                   kprof["obs_kernel_ms"], obs_bytes),
@@ -403,7 +403,7 @@ def run_gpu_arm(args) -> int:
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_env_step": bytes_per, "kernel_ms_avg": kern_avg,
-                         "scope": "one step = step kernel + observation kernel + reset kernel "
+                         "scope": "one step = controller pass + step kernel + observation kernel + reset kernel "
                                   "(SURVEY.md 8(d) bytes per env-step x envs / step time)",
                          "kernels": kernels,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks
@@ -411,7 +411,10 @@ def run_gpu_arm(args) -> int:
             "e2e": {"value": e2e_value, "unit": "env-steps/s",
                     "h2d_bytes_per_step": per * N * 8,
                     "d2h_bytes_per_step": per * N * 4 + 2 * per},
-            "gpu_launches": 3 * args.steps,
+            # K1, K2, K3 per step, plus K0 (the heuristic-controller pass) when
+            # the batch has one envs-per-warp layout (N <= 32) and it is enabled
+            "gpu_launches": (3 + (1 if N <= 32 and os.environ.get("TABX_NO_K0") != "1"
+                                  else 0)) * args.steps,
             "clocks": clk.summary(),
             "episode_stats": stats,
         }

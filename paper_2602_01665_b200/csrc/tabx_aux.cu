@@ -263,6 +263,11 @@ __global__ void derive_kernel(const tabx_config* __restrict__ cfgs, DerivedCfg* 
       }
       D->n_ally = na;
       D->n_enemy = ne;
+      int nh = 0;
+      for (int i = 0; i < C->n_units && i < 32; ++i)
+        if (C->active[i] && C->controller[C->team[i] ? 1 : 0] == TABX_CTRL_HEURISTIC)
+          D->hlist[nh++] = (uint8_t)i;
+      D->n_heur = nh;
     }
   }
 }

@@ -12,6 +12,7 @@
 
 namespace tabx {
 cudaError_t launch_lanes(const Params& P, int W, int sm_count, cudaStream_t stream, int* grid);
+cudaError_t launch_ctrl_w1(const Params& P, int nh, int sm_count, cudaStream_t stream);
 cudaError_t launch_emit(const Params& P, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
                             int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream);
@@ -58,6 +59,10 @@ struct tabx_handle {
   int auto_reset = 0;
   int sm_count = 148;
   bool any_external = false;
+  // K0 (heuristic controller pass, W == 1): per-unit actions, and the
+  // heuristic units per env over the config table (recounted when it changes)
+  int8_t* ctrl_act = nullptr;
+  int cfg_version = 0, ctrl_version = -1, ctrl_nh = 0;
   std::vector<tabx_config> cfg_host;  // host mirror of the table rows
   std::vector<char> cfg_host_ok;       // 0: row written on the device (tabx_levels)
   int cfg_cap = TABX_MAX_CONFIGS;
@@ -144,7 +149,31 @@ static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
   P.G = h->G;
   P.auto_reset = h->auto_reset;
   P.mode = mode;
+  P.ctrl_act = nullptr;
+  P.ctrl_nh = 0;
   return P;
+}
+
+// Heuristic-controlled active units per env among the first 32, maximised
+// over the config table (rows written on the device count as all 32).
+static int ctrl_units(tabx_handle* h) {
+  if (h->ctrl_version == h->cfg_version) return h->ctrl_nh;
+  const int lim = h->N < 32 ? h->N : 32;
+  int nh = 0;
+  for (size_t k = 0; k < h->cfg_host.size(); ++k) {
+    if (!h->cfg_host_ok[k]) {
+      nh = lim;
+      break;
+    }
+    const tabx_config& c = h->cfg_host[k];
+    int n = 0;
+    for (int i = 0; i < lim; ++i)
+      if (c.active[i] && c.controller[c.team[i] ? 1 : 0] == TABX_CTRL_HEURISTIC) ++n;
+    if (n > nh) nh = n;
+  }
+  h->ctrl_nh = nh;
+  h->ctrl_version = h->cfg_version;
+  return nh;
 }
 
 static int check_outputs(const tabx_outputs* out) {
@@ -168,6 +197,7 @@ static int find_or_add_config(tabx_handle* h, const tabx_config* c, int32_t* idx
     return fail(TABX_E_CAPACITY, "config table full");
   h->cfg_host.push_back(*c);
   h->cfg_host_ok.push_back(1);
+  ++h->cfg_version;
   const size_t k = h->cfg_host.size() - 1;
   TABX_CUDA(cudaMemcpyAsync(h->cfg_dev + k, c, sizeof(tabx_config), cudaMemcpyHostToDevice,
                             h->stream),
@@ -235,7 +265,7 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
          o_ub = take(U), o_vis = take(4 * U * W),
          o_atk = take(4 * U * W), o_se = take(4 * B), o_sw = take(4 * B), o_sf = take(4 * B),
          o_stie = take(4 * B), o_sel = take(4 * B), o_sl = take(8 * B), o_sr = take(8 * B),
-         o_sync = take(sizeof(Sync)), o_stats = take(8 * TABX_NUM_STATS);
+         o_sync = take(sizeof(Sync)), o_stats = take(8 * TABX_NUM_STATS), o_ctl = take(U);
   cudaError_t e = cudaMalloc(&h->arena, off);
   if (e != cudaSuccess) {
     delete h;
@@ -284,6 +314,9 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   st.st_ret = (double*)(a + o_sr);
   h->sync = (Sync*)(a + o_sync);
   h->stats_dev = (double*)(a + o_stats);
+  // K0 is the default for W == 1; TABX_NO_K0=1 keeps the decision inside K1
+  const char* no_k0 = getenv("TABX_NO_K0");
+  if (W == 1 && !(no_k0 && no_k0[0] == '1')) h->ctrl_act = (int8_t*)(a + o_ctl);
 
   int rc = TABX_OK;
   for (int k = 0; k < n_configs; ++k) {
@@ -386,6 +419,14 @@ int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
     h->prof_next = (slot + 1) % tabx_handle::PROF_SLOTS;
     ++h->prof_pending;
     cudaEventRecord(ev[0], h->stream);
+  }
+  if (h->ctrl_act) {
+    const int nh = ctrl_units(h);
+    if (nh > 0) {
+      P.ctrl_act = h->ctrl_act;
+      P.ctrl_nh = nh;
+      TABX_CUDA(launch_ctrl_w1(P, nh, h->sm_count, h->stream), "controller launch");
+    }
   }
   TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "step launch");
   if (ev) cudaEventRecord(ev[1], h->stream);
@@ -539,6 +580,7 @@ int tabx_levels(tabx_handle* h, int32_t op, const tabx_level_spec* spec, double 
     h->cfg_host_ok.resize(end, 0);
   }
   for (size_t k = (size_t)dst_first; k < end; ++k) h->cfg_host_ok[k] = 0;
+  ++h->cfg_version;
   return TABX_OK;
 }
 

@@ -520,15 +520,15 @@ constexpr int SA_ACT_MASK = 0xff, SA_HAS = 0x100, SA_MEMOK = 0x200, SA_TGT_SHIFT
 #else
 #define TABX_SCRIPTED_QUAL __device__ __noinline__
 #endif
-template <int W>
-TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
-                               int N, int Z, double hd, double cd, double step,
-                               uint32_t mask7, double u_explore, double u_pick,
-                               double eps, double xi, uint32_t bush_m, double mx, double my,
-                               bool memv) {
-  // everything arrives by value (scalars in registers, the unit's vis/atk rows
-  // in S.vis / S.atk): reference parameters of a non-inlined call would force
-  // the caller's copies into local memory
+// SV: the env view the decision reads (EnvSmem<W> in K1; CtrlView in K0):
+// px, py, ch, sh, rad, mh, uf, zin, the unit's vis / atk rows, m_active,
+// m_alive.
+template <int W, class SV>
+__device__ __forceinline__ int scripted_body(const SV& S, const tabx_config* __restrict__ C, int i,
+                                             int N, int Z, double hd, double cd, double step,
+                                             uint32_t mask7, double u_explore, double u_pick,
+                                             double eps, double xi, uint32_t bush_m, double mx,
+                                             double my, bool memv) {
   TABX_PHASE_BEGIN();
   const UnitStatic U = load_static(C, i, true);
   const uint32_t* vis = &S.vis[i * W];
@@ -632,6 +632,19 @@ TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* _
   if (u_explore < eps) act = kth_legal(mask7, u_pick);
   // packed result: action, memory update (has -> remember tgt; memv = has || mem_ok)
   return act | (has ? SA_HAS : 0) | (mem_ok ? SA_MEMOK : 0) | (tgt << SA_TGT_SHIFT);
+}
+
+// K1's out-of-line call: everything arrives by value (scalars in registers,
+// the unit's vis/atk rows in S.vis / S.atk): reference parameters of a
+// non-inlined call would force the caller's copies into local memory
+template <int W>
+TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* __restrict__ C, int i,
+                                       int N, int Z, double hd, double cd, double step,
+                                       uint32_t mask7, double u_explore, double u_pick,
+                                       double eps, double xi, uint32_t bush_m, double mx,
+                                       double my, bool memv) {
+  return scripted_body<W>(S, C, i, N, Z, hd, cd, step, mask7, u_explore, u_pick, eps, xi, bush_m,
+                          mx, my, memv);
 }
 
 // ---------------------------------------------------------------- lane ---
@@ -885,7 +898,10 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const bool heur = free_u && ctrl == TABX_CTRL_HEURISTIC;
   int act = A_NOOP;
   if (free_u && P.actions) act = (int)P.actions[u];
-  if (env_any<W>(heur, S, i)) {
+  if (W == 1 && P.ctrl_act != nullptr && !refresh && DC->n_heur <= P.ctrl_nh) {
+    // K0 made the decision (its memory update is in the state read above)
+    if (heur) act = (int)P.ctrl_act[u];
+  } else if (env_any<W>(heur, S, i)) {
     // cached vis/atk of the previous stage 8, or fresh after a batch refill
     if (refresh) {
       cache_row_of<W>(S, i, N, U, bush_m);

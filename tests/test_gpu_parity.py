@@ -375,3 +375,43 @@ def test_two_word_rows_with_zones_match_oracle():
         bad = compare_outputs(g, o, f"W=2 step {t}")
         bad += compare_state(gpu.export_state(), ora.sim, f"W=2 step {t}")
         assert not bad, "\n".join(bad[:10])
+
+
+def test_controller_pass_mixed_heuristic_counts():
+    """K0 (the packed heuristic-controller pass ahead of K1) over a batch whose
+    configs have 10 and 20 heuristic units per env: packing follows the
+    largest count, every env matches the oracle."""
+    a = builtin_scenario("c3_10v10_terrain").with_controllers(ally="random",
+                                                              enemy="heuristic:medium")
+    b = builtin_scenario("c3_10v10_terrain").scripted()
+    configs = [a, b, b, a, a, b, a, a] * 6
+    seeds = np.arange(len(configs), dtype=np.uint64) * 31 + 5
+    gpu = BatchSim(configs, seeds, auto_reset=True, device="cuda:0")
+    ora = orc.OracleBatchSim(configs, seeds, auto_reset=True)
+    for t in range(1, 60):
+        o = ora.step(None)
+        g = gpu.step(None)
+        bad = compare_outputs(g, o, f"k0 mixed t={t}") + compare_state(gpu.export_state(), ora.sim,
+                                                                       f"k0 mixed t={t}")
+        assert not bad, "\n".join(bad[:10])
+
+
+def test_controller_pass_equals_in_kernel_controller(monkeypatch):
+    """Full-size C3: the K0 decision path and K1's in-kernel controller
+    (TABX_NO_K0=1, read when the batch is created) give identical
+    observations and state step for step."""
+    sc = builtin_scenario("c3_10v10_terrain")
+    B = 32768
+    seeds = np.arange(B, dtype=np.uint64) + 3
+    sims = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("TABX_NO_K0", flag)
+        sims.append(BatchSim([sc] * B, seeds, auto_reset=True, device="cuda:0",
+                             interactions=False))
+    for t in range(40):
+        outs = [s.step(None) for s in sims]
+        assert torch.equal(outs[0].observations, outs[1].observations), t
+        assert torch.equal(outs[0].rewards, outs[1].rewards), t
+    s0, s1 = (s.export_state() for s in sims)
+    for k in ("pos", "health", "heading", "alive", "mem_pos", "mem_valid"):
+        assert torch.equal(s0[k], s1[k]), k

@@ -1,5 +1,3 @@
 #!/bin/bash
-# Scratch job for gpurun (edited per experiment): GPU tests + A/B timing.
 python -c "import sys; sys.path.insert(0,'.'); from paper_2602_01665_b200 import _native as n; n.lib()" || { echo "default lib broken"; exit 1; }
-python -m pytest tests -m gpu -x -q > gpurun_out/pt.log 2>&1; tail -2 gpurun_out/pt.log
-REPS=3 bash tools/kab.sh default
+REPS=3 bash tools/kab.sh default variants/k0mb6.so variants/k0mb8.so

@@ -8,8 +8,8 @@ The ncu command is the recipe's launch pass with DRAM bytes added:
         --clock-control none --csv python bench.py --steps 2 --warmup 1 --no-cpu \
         --no-e2e --rollout-envs 0 --envs 65536
 The traffic file records the DRAM bytes per env-step of one whole step (the
-step kernel launch given and the two launches after it: observation and
-reset kernels), which bench.py reports as ``roofline.traffic``.
+controller-pass / step kernel launch given through the reset kernel that
+ends the step), which bench.py reports as ``roofline.traffic``.
 """
 from __future__ import annotations
 
@@ -46,7 +46,13 @@ def main(argv) -> int:
             rd, wr = d.get("dram__bytes_read.sum", 0.0), d.get("dram__bytes_write.sum", 0.0)
             pct = 100.0 * (rd + wr) / (ns * 1e-9) / (PEAK_GBS * 1e9) if ns else 0.0
             fh.write(f"{k},{d['kernel']},{ns / 1e6:.3f},{pct:.1f},{rd / 1e6:.1f},{wr / 1e6:.1f}\n")
-    step = [data[first + j] for j in range(3)]
+    # one step: the launch given (K0, or K1 when K0 does not run) through the
+    # reset kernel (lane_kernel<W, EPB, 3>) that ends it
+    step = []
+    for k in sorted(x for x in data if x >= first):
+        step.append(data[k])
+        if data[k]["kernel"].rstrip().endswith(", 3>"):
+            break
     total = sum(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
                 for d in step)
     per_kernel = {f"{first + j}:{d['kernel']}": round((d.get("dram__bytes_read.sum", 0.0) +
@@ -55,7 +61,7 @@ def main(argv) -> int:
     doc = {"bytes_per_env_step": round(total / envs), "algorithmic_bytes_per_env_step": 36295,
            "per_kernel": per_kernel,
            "source": f"ncu dram__bytes_read.sum + dram__bytes_write.sum of one step (launches "
-                     f"{first}-{first + 2} of {out_csv}) at {envs:,} envs",
+                     f"{first}-{first + len(step) - 1} of {out_csv}) at {envs:,} envs",
            "scenario": "c3_10v10_terrain"}
     with open(traffic_json, "w", encoding="utf-8") as fh:
         json.dump(doc, fh, indent=1)
