@@ -411,9 +411,10 @@ def run_gpu_arm(args) -> int:
             "e2e": {"value": e2e_value, "unit": "env-steps/s",
                     "h2d_bytes_per_step": per * N * 8,
                     "d2h_bytes_per_step": per * N * 4 + 2 * per},
-            # K1, K2, K3 per step, plus K0 (the heuristic-controller pass) when
-            # the batch has one envs-per-warp layout (N <= 32) and it is enabled
-            "gpu_launches": (3 + (1 if N <= 32 and os.environ.get("TABX_NO_K0") != "1"
+            # K1, K2, K3 per step, plus the refresh check and K0 (the
+            # heuristic-controller pass) when the batch has the env-per-warp
+            # layout (N <= 32) and K0 is enabled
+            "gpu_launches": (3 + (2 if N <= 32 and os.environ.get("TABX_NO_K0") != "1"
                                   else 0)) * args.steps,
             "clocks": clk.summary(),
             "episode_stats": stats,

@@ -150,7 +150,6 @@ static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
   P.auto_reset = h->auto_reset;
   P.mode = mode;
   P.ctrl_act = nullptr;
-  P.ctrl_nh = 0;
   return P;
 }
 
@@ -423,9 +422,13 @@ int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
   if (h->ctrl_act) {
     const int nh = ctrl_units(h);
     if (nh > 0) {
+      // K0 path: a pending batch refresh is materialised first (the rows K0
+      // reads), then K0 decides, then the controller-free step kernel
+      Params R = make_params(h, MODE_REFRESH, nullptr, nullptr);
+      TABX_CUDA(launch_lanes(R, h->W, h->sm_count, h->stream, nullptr), "refresh launch");
       P.ctrl_act = h->ctrl_act;
-      P.ctrl_nh = nh;
       TABX_CUDA(launch_ctrl_w1(P, nh, h->sm_count, h->stream), "controller launch");
+      P.mode = MODE_STEP_K0;
     }
   }
   TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "step launch");

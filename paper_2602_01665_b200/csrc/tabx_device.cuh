@@ -91,7 +91,10 @@ struct DerivedCfg {
   float zglob[TABX_MAX_ZONES * TABX_ZONE_DIM];
 };
 
-enum Mode : int { MODE_STEP = 0, MODE_INIT = 1, MODE_REFRESH = 2, MODE_RESET = 3 };
+// MODE_STEP_K0: the step kernel when K0 (the heuristic-controller pass) made
+// the heuristic decisions; it carries no controller code of its own
+enum Mode : int { MODE_STEP = 0, MODE_INIT = 1, MODE_REFRESH = 2, MODE_RESET = 3, MODE_STEP_K0 = 4 };
+__host__ __device__ constexpr bool is_step_mode(int m) { return m == MODE_STEP || m == MODE_STEP_K0; }
 
 struct Params {
   DevState st;
@@ -107,7 +110,6 @@ struct Params {
   // K0 (heuristic controller pass, W == 1): its action per unit, or nullptr
   // when K1 runs the controller itself
   int8_t* ctrl_act;
-  int ctrl_nh;  // K0's heuristic units per env; envs with more are K1's
 };
 
 __device__ __noinline__ static bool zone_exact(double ex, double ey, double ax, double ay) {

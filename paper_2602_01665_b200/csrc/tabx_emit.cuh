@@ -410,7 +410,7 @@ template <int W, int EPW>
 __global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS)
     emit_kernel(const Params P, int R, int SF) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  if (P.mode == MODE_STEP && P.sync->err_index != NO_ERROR) return;
+  if (is_step_mode(P.mode) && P.sync->err_index != NO_ERROR) return;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const EmitScratch<W> X =
       emit_scratch<W>(smem_raw + (size_t)w * emit_warp_bytes<W>(P.N, P.Z, R, SF), P.N, P.Z, R);

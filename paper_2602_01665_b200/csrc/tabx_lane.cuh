@@ -690,7 +690,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     ivy = iv.y;
     // realized velocity is output-only (written back only by running lanes);
     // the scripted-controller memory only exists for heuristic-team units
-    if (M == MODE_STEP && C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC) {
+    if (is_step_mode(M) && C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC) {
       const double2 m = st.mem_pos[u];
       mx = m.x;
       my = m.y;
@@ -815,7 +815,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     return;
   }
 
-  if (M != MODE_STEP) {
+  if (!is_step_mode(M)) {
     // init_output / refresh_caches (environment.py:147-151, :351-374)
     publish();
     build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
@@ -898,7 +898,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const bool heur = free_u && ctrl == TABX_CTRL_HEURISTIC;
   int act = A_NOOP;
   if (free_u && P.actions) act = (int)P.actions[u];
-  if (W == 1 && P.ctrl_act != nullptr && !refresh && DC->n_heur <= P.ctrl_nh) {
+  if (M == MODE_STEP_K0) {
     // K0 made the decision (its memory update is in the state read above)
     if (heur) act = (int)P.ctrl_act[u];
   } else if (env_any<W>(heur, S, i)) {
@@ -1320,15 +1320,16 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
 
   uint32_t step_no = 0;
   bool refresh = false;
-  if (M == MODE_STEP || M == MODE_RESET) {
+  if (is_step_mode(M) || M == MODE_RESET) {
     if (P.sync->err_index != NO_ERROR) return;  // an action violated the mask: no mutation
     step_no = P.sync->step;
     refresh = P.sync->refresh[step_no % 3] != 0;
-    if (M == MODE_STEP && blockIdx.x == 0 && threadIdx.x == 0)
+    if (is_step_mode(M) && blockIdx.x == 0 && threadIdx.x == 0)
       P.sync->refresh[(step_no + 2) % 3] = 0;
   } else if (M == MODE_REFRESH) {
     step_no = P.sync->step;
     refresh = P.sync->refresh[step_no % 3] != 0;
+    if (!refresh) return;  // nothing pending: the cached rows stand
   }
   const int g = threadIdx.x / (32 * W);
   const int i = threadIdx.x % (32 * W);
@@ -1399,6 +1400,11 @@ template <int W, int EPB>
 cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream, int* grid_out) {
   switch (P.mode) {
     case MODE_STEP: return launch_lanes_m<W, EPB, MODE_STEP>(P, sm_count, stream, grid_out);
+    case MODE_STEP_K0:
+      if constexpr (W == 1)
+        return launch_lanes_m<W, EPB, MODE_STEP_K0>(P, sm_count, stream, grid_out);
+      else
+        return cudaErrorInvalidValue;
     case MODE_INIT: return launch_lanes_m<W, EPB, MODE_INIT>(P, sm_count, stream, grid_out);
     case MODE_REFRESH:
       return launch_lanes_m<W, EPB, MODE_REFRESH>(P, sm_count, stream, grid_out);

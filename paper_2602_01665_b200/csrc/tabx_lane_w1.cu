@@ -10,8 +10,9 @@ namespace tabx {
 // per-env view staged in shared memory.  Same inputs as K1's in-kernel call
 // (the pre-step state, the cached vis/atk rows), so the same decision; the
 // action goes to P.ctrl_act and the scripted-controller memory straight to
-// the state, where K1 reads it.  Steps that refresh the caches (a batch
-// refill) and steps with a latched action error leave it to K1.
+// the state, where K1 reads it.  On a step that refreshes the caches (a batch
+// refill) the refresh kernel has rewritten the rows first; a step with a
+// latched action error is skipped (no mutation).
 struct CtrlView {
   double px[32], py[32], ch[32], sh[32], rad[32], mh[32];
   uint32_t uf[32], zin[32], vis[32], atk[32];
@@ -23,7 +24,6 @@ struct CtrlView {
 #endif
 __global__ void __launch_bounds__(128, TABX_K0_MINB) ctrl_kernel(const Params P, int G, int NH) {
   if (P.sync->err_index != NO_ERROR) return;
-  if (P.sync->refresh[P.sync->step % 3] != 0) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   CtrlView* V = reinterpret_cast<CtrlView*>(smem_raw) + wib * G;
@@ -70,9 +70,11 @@ __global__ void __launch_bounds__(128, TABX_K0_MINB) ctrl_kernel(const Params P,
       const int32_t cf = st.cfg[b];
       const tabx_config* __restrict__ C = P.cfgs + cf;
       const DerivedCfg* __restrict__ DC = P.dcfgs + cf;
-      // (an env with more heuristic units than the launch packs is K1's)
-      if (k < DC->n_heur && DC->n_heur <= NH && !(st.flags[b] & F_DONE)) {
-        const int i = DC->hlist[k];
+      // an env with more heuristic units than the launch packs (a config
+      // added after a graph capture) takes extra rounds on the same lanes
+      const int nheur = (st.flags[b] & F_DONE) ? 0 : DC->n_heur;
+      for (int kk = k; kk < nheur; kk += NH) {
+        const int i = DC->hlist[kk];
         const int64_t u = b * N + i;
         const uint8_t ub = st.ubits[u];
         if (ub & U_ALIVE) {  // free: alive, active (hlist), lane running
