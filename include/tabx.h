@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define TABX_ABI_VERSION 2
+#define TABX_ABI_VERSION 3
 
 #define TABX_MAX_UNITS 256
 #define TABX_MAX_ZONES 32
@@ -137,6 +137,13 @@ typedef struct tabx_outputs {
   float* final_observations;  /* [B, N, obs_dim]          */
   float* final_global_state;  /* [B, global_dim]          */
   uint8_t* reset_mask;        /* [B]                      */
+  /* Optional policy feed (not in the reference): the current observation
+   * rows again as bfloat16 (round to nearest even), row stride
+   * observations_bf16_ld elements (>= obs_dim, a multiple of 8; the columns
+   * from obs_dim on are zero), i.e. 16-byte aligned rows a policy network
+   * reads directly.  Lanes that auto-reset get their fresh observation. */
+  void* observations_bf16;      /* [B, N, observations_bf16_ld] bf16 */
+  int64_t observations_bf16_ld;
 } tabx_outputs;
 
 /*

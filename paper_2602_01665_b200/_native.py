@@ -12,7 +12,7 @@ MAX_UNITS = 256
 MAX_ZONES = 32
 NUM_ACTIONS = 7
 NUM_STATS = 8
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 OK = 0
 E_ARGUMENT, E_CUDA, E_ACTION_MASK, E_SHAPE, E_ALIGNMENT, E_CAPACITY = 1, 2, 3, 4, 5, 6
@@ -54,7 +54,9 @@ OUTPUT_FIELDS = ("observations", "global_state", "rewards", "action_mask", "term
 
 
 class TabxOutputs(ct.Structure):
-    _fields_ = [(name, ct.c_void_p) for name in OUTPUT_FIELDS]
+    # + the optional bfloat16 policy feed (tabx.h)
+    _fields_ = [(name, ct.c_void_p) for name in OUTPUT_FIELDS] + [
+        ("observations_bf16", ct.c_void_p), ("observations_bf16_ld", ct.c_int64)]
 
 
 STATE_FIELDS = ("seed", "episode", "t", "pos", "heading", "vel", "imp_dv", "health", "cooldown",

@@ -175,11 +175,16 @@ static int ctrl_units(tabx_handle* h) {
   return nh;
 }
 
-static int check_outputs(const tabx_outputs* out) {
+static int check_outputs(const tabx_outputs* out, int D) {
   if (!out) return TABX_OK;
   const float* ptrs[2] = {out->observations, out->final_observations};
   for (const float* p : ptrs)
     if (p && (((uintptr_t)p) & 15u)) return fail(TABX_E_ALIGNMENT, "observation buffer must be 16-byte aligned");
+  if (out->observations_bf16 && ((((uintptr_t)out->observations_bf16) & 15u) ||
+                                 (out->observations_bf16_ld & 7) ||
+                                 out->observations_bf16_ld < D))
+    return fail(TABX_E_ALIGNMENT,
+                "bfloat16 observation rows must be 16-byte aligned (ld a multiple of 8)");
   return TABX_OK;
 }
 
@@ -382,7 +387,7 @@ int tabx_dims(const tabx_handle* h, int64_t* batch, int32_t* n_units, int32_t* n
 
 int tabx_init_output(tabx_handle* h, const tabx_outputs* out) {
   if (!h) return fail(TABX_E_ARGUMENT, "null handle");
-  int rc = check_outputs(out);
+  int rc = check_outputs(out, h->D);
   if (rc) return rc;
   DeviceGuard guard(h->device);
   Params P = make_params(h, MODE_INIT, nullptr, out);
@@ -396,7 +401,7 @@ int tabx_init_output(tabx_handle* h, const tabx_outputs* out) {
 
 int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
   if (!h) return fail(TABX_E_ARGUMENT, "null handle");
-  int rc = check_outputs(out);
+  int rc = check_outputs(out, h->D);
   if (rc) return rc;
   DeviceGuard guard(h->device);
   if (actions && h->any_external) {
@@ -444,7 +449,7 @@ int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
 int tabx_reset_env(tabx_handle* h, int64_t b, const tabx_config* config, uint64_t seed,
                    int32_t has_seed, const tabx_outputs* out) {
   if (!h || b < 0 || b >= h->B) return fail(TABX_E_ARGUMENT, "tabx_reset_env: bad lane");
-  int rc = check_outputs(out);
+  int rc = check_outputs(out, h->D);
   if (rc) return rc;
   DeviceGuard guard(h->device);
   if (config) {

@@ -9,6 +9,7 @@
 // few at a time in shared memory and streams them out with double-buffered
 // TMA bulk stores.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -191,11 +192,14 @@ __device__ __forceinline__ int nth_bit(uint32_t w, int n) {
 // tensor -- cost only the fill.  `buf` (the stage buffer to fill next)
 // persists across the envs a warp emits so the buffer rotation never waits
 // on the store just issued; drain = wait for every store before returning.
-template <int W>
+// o16 (optional): the bfloat16 policy-feed copy of the observation rows,
+// row stride ld16 (tabx.h observations_bf16), written from the same stage.
+template <int W, bool F16 = false>
 __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
                           float* __restrict__ glob, int64_t b, int N, int Z, int D, int G, int R,
                           int SF, const tabx_config* __restrict__ C,
-                          const DerivedCfg* __restrict__ DC, int lane, int& buf, bool drain) {
+                          const DerivedCfg* __restrict__ DC, int lane, int& buf, bool drain,
+                          __nv_bfloat16* __restrict__ o16 = nullptr, int ld16 = 0) {
   const EmitEnv<W>& E = X.E;
   const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
   const int M = N - 1;
@@ -223,7 +227,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
   const double rel_c = rel_on ? (rel_ax ? C->zone_cy[rel_z] : C->zone_cx[rel_z]) : 0.0;
   const double rel_f = rel_ax ? fh : fw, rel_rf = rel_ax ? rh : rw;
   const int rel_off = rel_rr * D + zoff + rel_z * TABX_ZONE_DIM + 3 + rel_ax;
-  if (obs) {
+  if (obs || (F16 && o16)) {
     for (int r0 = 0; r0 < N; r0 += R) {
       const int nr = min(R, N - r0);
       const int64_t gs = (b * N + r0) * (int64_t)D;
@@ -334,7 +338,35 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
       }
       fence_proxy_async();
       __syncwarp();
-      flush_stage(obs, gs, nr * D, st, lane);
+      if (obs) flush_stage(obs, gs, nr * D, st, lane);
+      if (F16 && o16) {
+        // 8 bfloat16 (16 bytes) per store, zero past obs_dim; the stage is
+        // only read, beside the bulk store reading it.  Rows start 8-byte
+        // aligned in the stage (D even), so float2 loads.
+        const int per_row = ld16 >> 3;
+        for (int rr = 0; rr < nr; ++rr) {
+          const float* src = row0 + rr * D;
+          __nv_bfloat16* dst = o16 + (b * N + r0 + rr) * (int64_t)ld16;
+          for (int c = lane; c < per_row; c += 32) {
+            const int c0 = c << 3;
+            __align__(16) __nv_bfloat162 v[4];
+            if ((D & 1) == 0 && ((pad + rr * D) & 1) == 0 && c0 + 8 <= D) {
+              const float2* s2 = reinterpret_cast<const float2*>(src + c0);
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const float2 f = s2[k];
+                v[k] = __floats2bfloat162_rn(f.x, f.y);
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                v[k] = __floats2bfloat162_rn(c0 + 2 * k < D ? src[c0 + 2 * k] : 0.0f,
+                                             c0 + 2 * k + 1 < D ? src[c0 + 2 * k + 1] : 0.0f);
+            }
+            *reinterpret_cast<uint4*>(dst + c0) = *reinterpret_cast<const uint4*>(v);
+          }
+        }
+      }
       buf ^= 1;
     }
   }
@@ -406,7 +438,7 @@ __device__ __forceinline__ EmitScratch<W> emit_scratch(unsigned char* base, int 
   return X;
 }
 
-template <int W, int EPW>
+template <int W, int EPW, bool F16>
 __global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS)
     emit_kernel(const Params P, int R, int SF) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -423,25 +455,29 @@ __global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS)
     const bool pending = (st.flags[b] & F_PEND) != 0;
     float* ob = pending ? P.out.final_observations : P.out.observations;
     float* gb = pending ? P.out.final_global_state : P.out.global_state;
-    if (!ob && !gb) continue;
+    // the policy feed always holds the current observation: K3 writes it for
+    // the lanes it resets
+    __nv_bfloat16* o16 = (F16 && !pending) ? (__nv_bfloat16*)P.out.observations_bf16 : nullptr;
+    if (!ob && !gb && !o16) continue;
     load_view<W>(X, st, b, P.N, P.Z, C, DC, lane);
-    emit_lane<W>(X, ob, gb, b, P.N, P.Z, P.D, P.G, R, SF, C, DC, lane, buf, false);
+    emit_lane<W, F16>(X, ob, gb, b, P.N, P.Z, P.D, P.G, R, SF, C, DC, lane, buf, false, o16,
+                      (int)P.out.observations_bf16_ld);
   }
   if (lane == 0) bulk_wait_all();
 }
 
-template <int W, int EPW>
-cudaError_t launch_emit_t(const Params& P, int sm_count, cudaStream_t stream) {
+template <int W, int EPW, bool F16>
+cudaError_t launch_emit_f(const Params& P, int sm_count, cudaStream_t stream) {
   const int R = emit_rows(P.N, P.D, W == 1 ? TABX_EMIT_BUDGET : 8192);
   const int SF = emit_stage_floats(P.N, P.D, P.G, R);
   const size_t smem = (size_t)EPW * emit_warp_bytes<W>(P.N, P.Z, R, SF);
   static size_t cached_smem = 0;
   static int per_sm = 0;
   if (smem != cached_smem) {
-    cudaError_t e = cudaFuncSetAttribute(emit_kernel<W, EPW>,
+    cudaError_t e = cudaFuncSetAttribute(emit_kernel<W, EPW, F16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_kernel<W, EPW>, 32 * EPW,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_kernel<W, EPW, F16>, 32 * EPW,
                                                       smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
@@ -451,8 +487,16 @@ cudaError_t launch_emit_t(const Params& P, int sm_count, cudaStream_t stream) {
   int64_t cap = (int64_t)sm_count * per_sm;
   int grid = (int)(need < cap ? need : cap);
   if (grid < 1) grid = 1;
-  emit_kernel<W, EPW><<<grid, 32 * EPW, smem, stream>>>(P, R, SF);
+  emit_kernel<W, EPW, F16><<<grid, 32 * EPW, smem, stream>>>(P, R, SF);
   return cudaGetLastError();
+}
+
+// The bfloat16 policy feed is its own instantiation: the plain observation
+// stream carries none of its code.
+template <int W, int EPW>
+cudaError_t launch_emit_t(const Params& P, int sm_count, cudaStream_t stream) {
+  return P.out.observations_bf16 ? launch_emit_f<W, EPW, true>(P, sm_count, stream)
+                                 : launch_emit_f<W, EPW, false>(P, sm_count, stream);
 }
 
 }  // namespace tabx

@@ -808,8 +808,13 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
       const EmitScratch<W> X = emit_scratch<W>(emit, N, Z, R);
       int buf = 0;
       load_view<W>(X, st, b, N, Z, C, DC, i);
-      emit_lane<W>(X, O.observations, O.global_state, b, N, Z, P.D, P.G, R, SF, C, DC, i, buf,
-                   true);
+      if (O.observations_bf16)
+        emit_lane<W, true>(X, O.observations, O.global_state, b, N, Z, P.D, P.G, R, SF, C, DC, i,
+                           buf, true, (__nv_bfloat16*)O.observations_bf16,
+                           (int)O.observations_bf16_ld);
+      else
+        emit_lane<W>(X, O.observations, O.global_state, b, N, Z, P.D, P.G, R, SF, C, DC, i, buf,
+                     true);
     }
     env_sync<W>();
     return;

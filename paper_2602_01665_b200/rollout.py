@@ -111,9 +111,18 @@ class Rollout:
             o.truncated = self.buf.truncated[t].data_ptr()
             o.done = self.sim._buf["done"].data_ptr()
             o.reset_mask = self.sim._buf["reset_mask"].data_ptr()
+            if self.policy is not None:
+                # the step's emitter also writes the policy's bf16 input rows
+                o.observations_bf16 = self._xin.data_ptr()
+                o.observations_bf16_ld = self.policy.in_dim
             self._outs.append(o)
         if store_obs:
             self.buf.observations[0].copy_(self.sim._buf["observations"])
+        if self.policy is not None:  # the start observation, once
+            nat.check(nat.lib().tabx_pack_bf16(
+                ct.c_void_p(self.sim._buf["observations"].data_ptr()), B * N, D,
+                self.policy.in_dim, ct.c_void_p(self._xin.data_ptr()),
+                ct.c_void_p(torch.cuda.current_stream(dev).cuda_stream)), "tabx_pack_bf16")
         self.graph = None
         self.use_graph = use_graph
 
@@ -124,15 +133,12 @@ class Rollout:
 
     def _step(self, t):
         mask = self.sim._buf["action_mask"]
-        obs = self._current_obs(t)
         L = nat.lib()
         stream = torch.cuda.current_stream(self.device).cuda_stream
         if self.policy is None:
             logits, bf16 = self._zero_logits, 0
         else:
-            nat.check(L.tabx_pack_bf16(ct.c_void_p(obs.data_ptr()), self.B * self.N, self.D,
-                                       self.policy.in_dim, ct.c_void_p(self._xin.data_ptr()),
-                                       ct.c_void_p(stream)), "tabx_pack_bf16")
+            # _xin: the current observation in bf16, written by the last step
             logits, bf16 = self.policy(self._xin).reshape(self.B * self.N, -1), 1
         nat.check(L.tabx_masked_sample(
             ct.c_void_p(logits.data_ptr()), bf16, logits.shape[-1], ct.c_void_p(mask.data_ptr()),

@@ -61,3 +61,29 @@ def test_uniform_and_argmax():
     a1, _ = sample(torch.zeros(M, 8, device="cuda"), mask, seed=7, step=5)
     a2, _ = sample(torch.zeros(M, 8, device="cuda"), mask, seed=7, step=6)
     assert not torch.equal(a1, a2)  # the step counter changes the noise
+
+
+def test_bf16_policy_feed_equals_packed_observations():
+    """The emitter's bfloat16 policy feed (tabx_outputs.observations_bf16, written
+    by K2 and, for auto-reset lanes, K3) equals tabx_pack_bf16 of the float32
+    observation after every step, across episode boundaries."""
+    from dataclasses import replace
+
+    from paper_2602_01665_b200.rollout import Rollout
+    from paper_2602_01665_b200.scenario import builtin_scenario
+    sc = replace(builtin_scenario("c3_10v10_terrain"), max_steps=7)
+    ro = Rollout(sc, 300, horizon=20, policy="mlp", device=0, use_graph=False)
+    B, N, D, Dp = ro.B, ro.N, ro.D, ro.policy.in_dim
+    ref = torch.empty(B, N, Dp, dtype=torch.bfloat16, device="cuda")
+    resets = 0
+    for t in range(ro.T):
+        ro._step(t)
+        obs = ro.buf.observations[t + 1]
+        nat.check(nat.lib().tabx_pack_bf16(
+            ct.c_void_p(obs.data_ptr()), B * N, D, Dp, ct.c_void_p(ref.data_ptr()),
+            ct.c_void_p(torch.cuda.current_stream().cuda_stream)), "tabx_pack_bf16")
+        torch.cuda.synchronize()
+        assert torch.equal(ro._xin.view(torch.int16), ref.view(torch.int16)), t
+        resets += int(ro.sim._buf["reset_mask"].sum())
+    assert resets > 0
+    ro.close()

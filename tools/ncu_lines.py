@@ -1,7 +1,7 @@
 """Aggregate an ncu SASS source page by CUDA source line.
 
 usage: python tools/ncu_lines.py <sass.csv from ncu --page source --print-source sass>
-                                 <nvdisasm -g -c listing> [top]
+                                 <nvdisasm -g -c listing> [top] [kernel-symbol substring]
 Prints the hottest source lines by executed warp instructions and stall samples.
 """
 import csv
@@ -10,7 +10,7 @@ import sys
 from collections import defaultdict
 
 
-def line_map(listing, fn="lane_kernel"):
+def line_map(listing, fn="lane_kernel"):  # fn: substring of the kernel symbol
     cur = None
     m = {}
     rx_line = re.compile(r'//## File "([^"]+)", line (\d+)')
@@ -36,7 +36,7 @@ def line_map(listing, fn="lane_kernel"):
 def main():
     sass, listing = sys.argv[1], sys.argv[2]
     top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
-    lm = line_map(listing)
+    lm = line_map(listing, sys.argv[4] if len(sys.argv) > 4 else "lane_kernel")
     rows = list(csv.reader(open(sass)))
     hdr = rows[1]
     ia, ie, isamp = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index(
