@@ -126,8 +126,10 @@ __device__ __forceinline__ uint32_t zone_bits(const tabx_config* __restrict__ C,
                                               const DerivedCfg* __restrict__ DC, int Z, double x,
                                               double y) {
   uint32_t bits = 0;
-  for (int z = 0; z < Z; ++z) {
-    if (C->zone_type[z] == TABX_ZONE_NONE) continue;
+  (void)Z;
+  // the typed zones (lava | bush | swamp) by their bits: no per-zone type load
+  for (uint32_t m = DC->lava_m | DC->bush_m | DC->swamp_m; m; m &= m - 1) {
+    const int z = __ffs(m) - 1;
     const double ex = x - C->zone_cx[z];
     const double ey = y - C->zone_cy[z];
     const double ax = ex * DC->rax[z], ay = ey * DC->ray[z];
