@@ -414,8 +414,8 @@ def run_gpu_arm(args) -> int:
             # K1, K2, K3 per step, plus the refresh check and K0 (the
             # heuristic-controller pass) when the batch has the env-per-warp
             # layout (N <= 32) and K0 is enabled
-            "gpu_launches": (3 + (2 if N <= 32 and os.environ.get("TABX_NO_K0") != "1"
-                                  else 0)) * args.steps,
+            "gpu_launches": (3 + (2 if N <= 32 and per >= int(os.environ.get("TABX_K0_MIN_ENVS", 4096))
+                                  and os.environ.get("TABX_NO_K0") != "1" else 0)) * args.steps,
             "clocks": clk.summary(),
             "episode_stats": stats,
         }

@@ -318,9 +318,14 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   st.st_ret = (double*)(a + o_sr);
   h->sync = (Sync*)(a + o_sync);
   h->stats_dev = (double*)(a + o_stats);
-  // K0 is the default for W == 1; TABX_NO_K0=1 keeps the decision inside K1
+  // K0 is the default for W == 1 from TABX_K0_MIN_ENVS lanes on (4096; below
+  // that the step is launch-latency bound and two extra launches cost more
+  // than K0 saves); TABX_NO_K0=1 keeps the decision inside K1 always
   const char* no_k0 = getenv("TABX_NO_K0");
-  if (W == 1 && !(no_k0 && no_k0[0] == '1')) h->ctrl_act = (int8_t*)(a + o_ctl);
+  const char* k0_min = getenv("TABX_K0_MIN_ENVS");
+  const int64_t k0_envs = k0_min ? atoll(k0_min) : 4096;
+  if (W == 1 && B >= k0_envs && !(no_k0 && no_k0[0] == '1'))
+    h->ctrl_act = (int8_t*)(a + o_ctl);
 
   int rc = TABX_OK;
   for (int k = 0; k < n_configs; ++k) {

@@ -33,8 +33,13 @@ def _pair(name):
     return case, gpu, ora
 
 
+@pytest.mark.parametrize("path", ["k0", "k1"])
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_golden_case_parity(name):
+def test_golden_case_parity(name, path, monkeypatch):
+    """path k0: heuristic decisions by the controller pass; k1: inside the
+    step kernel (TABX_NO_K0=1, the path below 4,096 lanes)."""
+    if path == "k1":
+        monkeypatch.setenv("TABX_NO_K0", "1")
     case, gpu, ora = _pair(name)
     gen = np.random.default_rng(case["external"]) if "external" in case else None
     resets = {int(k): v for k, v in case.get("resets", {}).items()}

@@ -1,3 +1,5 @@
 #!/bin/bash
 python -c "import sys; sys.path.insert(0,'.'); from paper_2602_01665_b200 import _native as n; n.lib()" || { echo "default lib broken"; exit 1; }
-REPS=3 bash tools/kab.sh variants/head.so default variants/bush.so
+python -m pytest tests -m gpu -x -q > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
+python bench.py --scenario c1 --no-cpu --rollout-envs 0 > gpurun_out/bench_c1.log 2>&1; tail -1 gpurun_out/bench_c1.log | cut -c1-120
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
