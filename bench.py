@@ -412,9 +412,8 @@ def run_gpu_arm(args) -> int:
                     "h2d_bytes_per_step": per * N * 8,
                     "d2h_bytes_per_step": per * N * 4 + 2 * per},
             # K1, K2, K3 per step, plus the refresh check and K0 (the
-            # heuristic-controller pass) when the batch has the env-per-warp
-            # layout (N <= 32) and K0 is enabled
-            "gpu_launches": (3 + (2 if N <= 32 and per >= int(os.environ.get("TABX_K0_MIN_ENVS", 4096))
+            # heuristic-controller pass) from 4,096 lanes on unless disabled
+            "gpu_launches": (3 + (2 if per >= int(os.environ.get("TABX_K0_MIN_ENVS", 4096))
                                   and os.environ.get("TABX_NO_K0") != "1" else 0)) * args.steps,
             "clocks": clk.summary(),
             "episode_stats": stats,

@@ -264,7 +264,7 @@ __global__ void derive_kernel(const tabx_config* __restrict__ cfgs, DerivedCfg* 
       D->n_ally = na;
       D->n_enemy = ne;
       int nh = 0;
-      for (int i = 0; i < C->n_units && i < 32; ++i)
+      for (int i = 0; i < C->n_units; ++i)
         if (C->active[i] && C->controller[C->team[i] ? 1 : 0] == TABX_CTRL_HEURISTIC)
           D->hlist[nh++] = (uint8_t)i;
       D->n_heur = nh;
@@ -307,6 +307,19 @@ __global__ void sincos_debug_kernel(const double* x, double* s, double* c, int64
     const sincos_t r = libm_sincos(x[k]);
     s[k] = r.s;
     c[k] = r.c;
+  }
+}
+
+cudaError_t launch_ctrl_w1(const Params& P, int nh, int sm_count, cudaStream_t stream);
+cudaError_t launch_ctrl_w2(const Params& P, int nh, int sm_count, cudaStream_t stream);
+cudaError_t launch_ctrl_w4(const Params& P, int nh, int sm_count, cudaStream_t stream);
+cudaError_t launch_ctrl_w8(const Params& P, int nh, int sm_count, cudaStream_t stream);
+cudaError_t launch_ctrl(const Params& P, int W, int nh, int sm_count, cudaStream_t stream) {
+  switch (W) {
+    case 1: return launch_ctrl_w1(P, nh, sm_count, stream);
+    case 2: return launch_ctrl_w2(P, nh, sm_count, stream);
+    case 4: return launch_ctrl_w4(P, nh, sm_count, stream);
+    default: return launch_ctrl_w8(P, nh, sm_count, stream);
   }
 }
 

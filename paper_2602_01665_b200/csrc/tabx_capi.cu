@@ -12,7 +12,7 @@
 
 namespace tabx {
 cudaError_t launch_lanes(const Params& P, int W, int sm_count, cudaStream_t stream, int* grid);
-cudaError_t launch_ctrl_w1(const Params& P, int nh, int sm_count, cudaStream_t stream);
+cudaError_t launch_ctrl(const Params& P, int W, int nh, int sm_count, cudaStream_t stream);
 cudaError_t launch_emit(const Params& P, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
                             int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream);
@@ -59,7 +59,7 @@ struct tabx_handle {
   int auto_reset = 0;
   int sm_count = 148;
   bool any_external = false;
-  // K0 (heuristic controller pass, W == 1): per-unit actions, and the
+  // K0 (heuristic controller pass): per-unit actions, and the
   // heuristic units per env over the config table (recounted when it changes)
   int8_t* ctrl_act = nullptr;
   int cfg_version = 0, ctrl_version = -1, ctrl_nh = 0;
@@ -153,11 +153,11 @@ static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
   return P;
 }
 
-// Heuristic-controlled active units per env among the first 32, maximised
-// over the config table (rows written on the device count as all 32).
+// Heuristic-controlled active units per env, maximised over the config
+// table (rows written on the device count as all N).
 static int ctrl_units(tabx_handle* h) {
   if (h->ctrl_version == h->cfg_version) return h->ctrl_nh;
-  const int lim = h->N < 32 ? h->N : 32;
+  const int lim = h->N;
   int nh = 0;
   for (size_t k = 0; k < h->cfg_host.size(); ++k) {
     if (!h->cfg_host_ok[k]) {
@@ -318,13 +318,13 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   st.st_ret = (double*)(a + o_sr);
   h->sync = (Sync*)(a + o_sync);
   h->stats_dev = (double*)(a + o_stats);
-  // K0 is the default for W == 1 from TABX_K0_MIN_ENVS lanes on (4096; below
+  // K0 is the default from TABX_K0_MIN_ENVS lanes on (4096; below
   // that the step is launch-latency bound and two extra launches cost more
   // than K0 saves); TABX_NO_K0=1 keeps the decision inside K1 always
   const char* no_k0 = getenv("TABX_NO_K0");
   const char* k0_min = getenv("TABX_K0_MIN_ENVS");
   const int64_t k0_envs = k0_min ? atoll(k0_min) : 4096;
-  if (W == 1 && B >= k0_envs && !(no_k0 && no_k0[0] == '1'))
+  if (B >= k0_envs && !(no_k0 && no_k0[0] == '1'))
     h->ctrl_act = (int8_t*)(a + o_ctl);
 
   int rc = TABX_OK;
@@ -437,7 +437,7 @@ int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
       Params R = make_params(h, MODE_REFRESH, nullptr, nullptr);
       TABX_CUDA(launch_lanes(R, h->W, h->sm_count, h->stream, nullptr), "refresh launch");
       P.ctrl_act = h->ctrl_act;
-      TABX_CUDA(launch_ctrl_w1(P, nh, h->sm_count, h->stream), "controller launch");
+      TABX_CUDA(launch_ctrl(P, h->W, nh, h->sm_count, h->stream), "controller launch");
       P.mode = MODE_STEP_K0;
     }
   }

@@ -80,10 +80,9 @@ struct DerivedCfg {
   double rucd[TABX_MAX_UNITS];        // 1/cooldown (0 if cooldown == 0)
   uint32_t lava_m, bush_m, swamp_m;   // zone-type bit masks
   int32_t n_ally, n_enemy;            // team roster sizes (active units)
-  // active units of heuristic-controlled teams among the first 32 (K0's work
-  // list, ascending unit index)
+  // active units of heuristic-controlled teams (K0's work list, ascending)
   int32_t n_heur;
-  uint8_t hlist[32];
+  uint8_t hlist[TABX_MAX_UNITS];
   // float32 zone blocks (perception.py:170-201), zeros for unused slots:
   // observation block with the two relative-position features left 0, and
   // the global-state block (absolute position / field size)
@@ -107,7 +106,7 @@ struct Params {
   int N, Z, D, G;
   int auto_reset;
   int mode;
-  // K0 (heuristic controller pass, W == 1): its action per unit, or nullptr
+  // K0 (heuristic controller pass): its action per unit, or nullptr
   // when K1 runs the controller itself
   int8_t* ctrl_act;
 };

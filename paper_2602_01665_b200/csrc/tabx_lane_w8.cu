@@ -2,6 +2,9 @@
 #include "tabx_lane.cuh"
 
 namespace tabx {
+cudaError_t launch_ctrl_w8(const Params& P, int nh, int sm_count, cudaStream_t stream) {
+  return launch_ctrl_t<8>(P, nh, sm_count, stream);
+}
 cudaError_t launch_lanes_w8(const Params& P, int sm_count, cudaStream_t stream, int* grid) {
   return launch_lanes_t<8, 1>(P, sm_count, stream, grid);
 }

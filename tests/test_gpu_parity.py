@@ -401,12 +401,13 @@ def test_controller_pass_mixed_heuristic_counts():
         assert not bad, "\n".join(bad[:10])
 
 
-def test_controller_pass_equals_in_kernel_controller(monkeypatch):
-    """Full-size C3: the K0 decision path and K1's in-kernel controller
-    (TABX_NO_K0=1, read when the batch is created) give identical
-    observations and state step for step."""
-    sc = builtin_scenario("c3_10v10_terrain")
-    B = 32768
+@pytest.mark.parametrize("scen,B", [("c3_10v10_terrain", 32768), ("c4_50v50", 2048)])
+def test_controller_pass_equals_in_kernel_controller(scen, B, monkeypatch):
+    """Large batches (C3: one env per warp; C4: W = 4, four warps per env):
+    the K0 decision path and K1's in-kernel controller (TABX_NO_K0=1, read
+    when the batch is created) give identical observations and state step
+    for step."""
+    sc = builtin_scenario(scen)
     seeds = np.arange(B, dtype=np.uint64) + 3
     sims = []
     for flag in ("0", "1"):
