@@ -1,9 +1,9 @@
 #!/bin/bash
-python -c "import sys; sys.path.insert(0,'.'); from paper_2602_01665_b200 import _native as n; n.lib()" || { echo "default lib broken"; exit 1; }
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
-REPS=2 bash tools/kab.sh variants/head.so default
-for lib in variants/head.so default; do
-  if [ "$lib" = default ]; then unset TABX_LIB; else export TABX_LIB=$PWD/$lib; fi
-  timeout 300 python bench.py --scenario c4 --no-cpu --no-e2e --rollout-envs 0 --steps 5 > gpurun_out/c4.log 2>&1
-  printf "c4 %-22s " "$lib"; python -c "import json; d=json.loads(open('gpurun_out/c4.log').read().strip().splitlines()[-1]); r=d['roofline']; print(round(d['value']/1e6,3), [(k['kernel'][:6], round(k['ms_avg'],3)) for k in r['kernels']])"
-done
+P="timeout 300 python tools/dual_probe.py"
+NSTREAMS=1 $P 262144 2>&1 | tail -1
+$P 2>&1 | tail -1
+TABX_CAP_K1=2 TABX_CAP_K2=1 $P 2>&1 | tail -1
+TABX_CAP_K1=2 TABX_CAP_K2=1 TABX_CAP_K0=2 $P 2>&1 | tail -1
+TABX_CAP_K1=3 TABX_CAP_K2=1 $P 2>&1 | tail -1
+TABX_CAP_K1=2 TABX_CAP_K2=2 $P 2>&1 | tail -1
+TABX_CAP_K1=1 TABX_CAP_K2=1 $P 2>&1 | tail -1
