@@ -1,8 +1,10 @@
 """Two C3 batches on two streams (a GPU's lanes as two shards): does the
 step logic of one overlap the observation stream of the other?
 
-    TABX_CAP_K1=2 TABX_CAP_K2=1 python tools/dual_probe.py [envs per batch] [steps]
+    NSTREAMS=2 python tools/dual_probe.py [envs per batch] [steps]
 Prints env-steps/s over both batches, device-timed (events on both streams).
+(The per-SM CTA caps of the experiment in DESIGN.md §6 were env knobs of the
+launchers at the time, removed since.)
 """
 from __future__ import annotations
 
@@ -40,6 +42,5 @@ for k, st in enumerate(streams):
     st.record_event(ev1[k])
 torch.cuda.synchronize()
 ms = max(ev0.elapsed_time(e) for e in ev1)
-print(f"streams={NS} envs/batch={B} caps K1={os.environ.get('TABX_CAP_K1', '-')} "
-      f"K2={os.environ.get('TABX_CAP_K2', '-')} K0={os.environ.get('TABX_CAP_K0', '-')}: "
+print(f"streams={NS} envs/batch={B}: "
       f"{NS * B * T / (ms / 1e3) / 1e6:.2f} M env-steps/s ({ms / T:.3f} ms per round)")
