@@ -388,7 +388,8 @@ def test_controller_pass_mixed_heuristic_counts():
     largest count, every env matches the oracle."""
     a = builtin_scenario("c3_10v10_terrain").with_controllers(ally="random",
                                                               enemy="heuristic:medium")
-    b = builtin_scenario("c3_10v10_terrain").scripted()
+    b = builtin_scenario("c3_10v10_terrain").with_controllers(ally="heuristic:expert",
+                                                              enemy="heuristic:medium")
     configs = [a, b, b, a, a, b, a, a] * 6
     seeds = np.arange(len(configs), dtype=np.uint64) * 31 + 5
     gpu = BatchSim(configs, seeds, auto_reset=True, device="cuda:0")
@@ -421,3 +422,47 @@ def test_controller_pass_equals_in_kernel_controller(scen, B, monkeypatch):
     s0, s1 = (s.export_state() for s in sims)
     for k in ("pos", "health", "heading", "alive", "mem_pos", "mem_valid"):
         assert torch.equal(s0[k], s1[k]), k
+
+
+def test_controller_pass_graph_after_config_growth():
+    """A CUDA graph captured while every config had 10 heuristic units keeps
+    its K0 packing (3 envs per warp) when reset_env later brings in a config
+    with 20: that env's units take a second round on the same lanes, and
+    every step still matches the oracle."""
+    import ctypes as ct
+
+    from paper_2602_01665_b200 import _native as nat
+    a = builtin_scenario("c3_10v10_terrain").with_controllers(ally="random",
+                                                              enemy="heuristic:medium")
+    b = builtin_scenario("c3_10v10_terrain").with_controllers(ally="heuristic:expert",
+                                                              enemy="heuristic:medium")
+    B = 48
+    seeds = np.arange(B, dtype=np.uint64) + 900
+    s = torch.cuda.Stream()
+    gpu = BatchSim([a] * B, seeds, auto_reset=True, device="cuda:0", stream=s)
+    ora = orc.OracleBatchSim([a] * B, seeds, auto_reset=True)
+    L = nat.lib()
+
+    def launch():
+        nat.check(L.tabx_step(gpu.handle, None, ct.byref(gpu._outs)), "tabx_step")
+
+    with torch.cuda.stream(s):
+        launch()  # eager warm-up step (the handle counts 10 heuristic units)
+    s.synchronize()
+    ora.step(None)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        launch()
+    for lane in (5, 17):
+        ora.reset_env(lane, b, seed=lane + 3)
+        gpu.reset_env(lane, b, seed=lane + 3)
+    for t in range(1, 25):
+        graph.replay()
+        torch.cuda.synchronize()
+        o = ora.step(None)
+        bad = compare_state(gpu.export_state(), ora.sim, f"graph t={t}")
+        got = gpu._buf["observations"].cpu().numpy()
+        if not np.array_equal(got, o["observations"].astype(np.float32)):
+            bad.append(f"graph t={t}: observations differ")
+        assert not bad, "\n".join(bad[:10])
+    gpu.close()

@@ -1,9 +1,3 @@
 #!/bin/bash
-P="timeout 300 python tools/dual_probe.py"
-NSTREAMS=1 $P 262144 2>&1 | tail -1
-$P 2>&1 | tail -1
-TABX_CAP_K1=2 TABX_CAP_K2=1 $P 2>&1 | tail -1
-TABX_CAP_K1=2 TABX_CAP_K2=1 TABX_CAP_K0=2 $P 2>&1 | tail -1
-TABX_CAP_K1=3 TABX_CAP_K2=1 $P 2>&1 | tail -1
-TABX_CAP_K1=2 TABX_CAP_K2=2 $P 2>&1 | tail -1
-TABX_CAP_K1=1 TABX_CAP_K2=1 $P 2>&1 | tail -1
+python -c "import sys; sys.path.insert(0,'.'); from paper_2602_01665_b200 import _native as n; n.lib()" || { echo "default lib broken"; exit 1; }
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
