@@ -690,7 +690,8 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     ivy = iv.y;
     // realized velocity is output-only (written back only by running lanes);
     // the scripted-controller memory only exists for heuristic-team units
-    if (is_step_mode(M) && C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC) {
+    // (under K0 the memory is K0's to update: K1 neither reads nor writes it)
+    if (M == MODE_STEP && C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC) {
       const double2 m = st.mem_pos[u];
       mx = m.x;
       my = m.y;
@@ -884,8 +885,15 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   }
 
   // ======================= step (environment.py:207-348) ==================
-  publish();
+  if (M == MODE_STEP_K0 && W == 1) {
+    // no in-kernel controller: the contact pass reads flags and radii (the
+    // positions are published after integration); stage 8 republishes all
+    S.rad[i] = U.rad;
+    S.uf[i] = (U.active ? UF_ACTIVE : 0u) | (alive ? UF_ALIVE : 0u);
+  } else {
+    publish();
     build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
+  }
   env_sync<W>();
 
   TABX_PHASE(0);
@@ -894,7 +902,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const uint32_t mask7 = ctl ? (0x1Fu | ((cd <= 0.0) ? 0x20u : 0u) | (C->enable_noop ? 0x40u : 0u))
                              : 0x40u;
   // effective speed after swamps at the pre-move position (arrays.py:338-343)
-  const double speff = U.speed * swamp_mult(C, Z, S.zin[i], swamp_m);
+  const double speff = U.speed * swamp_mult(C, Z, zin, swamp_m);
   TABX_PHASE(9);
   // 2. action resolution (environment.py:154-204)
   const int team = U.enemy ? 1 : 0;
@@ -1277,7 +1285,8 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     st.health[u] = hp;
     st.cooldown[u] = cd;
     st.reveal[u] = rv;
-    if (C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC) st.mem_pos[u] = make_double2(mx, my);
+    if (M == MODE_STEP && C->controller[U.enemy ? 1 : 0] == TABX_CTRL_HEURISTIC)
+      st.mem_pos[u] = make_double2(mx, my);
     st.hcs[u] = make_double2(ch, sh);
     st.zbits[u] = zin;
     st.ubits[u] = (alive ? U_ALIVE : 0) | (memv ? U_MEMV : 0);
