@@ -885,11 +885,17 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   }
 
   // ======================= step (environment.py:207-348) ==================
-  if (M == MODE_STEP_K0 && W == 1) {
+  if (M == MODE_STEP_K0) {
     // no in-kernel controller: the contact pass reads flags and radii (the
-    // positions are published after integration); stage 8 republishes all
+    // positions are published after integration) and, W > 1, the active set;
+    // stage 8 republishes everything
     S.rad[i] = U.rad;
     S.uf[i] = (U.active ? UF_ACTIVE : 0u) | (alive ? UF_ALIVE : 0u);
+    if (W > 1) {
+      uint32_t m[W];
+      env_ballot<W>(valid && U.active, S, i, m);
+      if ((i & 31) == 0) S.m_active[i >> 5] = m[i >> 5];
+    }
   } else {
     publish();
     build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
