@@ -125,6 +125,11 @@ __device__ __forceinline__ void load_view(const EmitScratch<W>& X, const DevStat
   __syncwarp();
 }
 
+// stage buffers per warp (2: fill one while the bulk store drains the other)
+#ifndef TABX_EMIT_NBUF
+#define TABX_EMIT_NBUF 2
+#endif
+
 // ---- TMA bulk stores (cp.async.bulk.global.shared::cta)
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -234,7 +239,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
       float* st = X.stage + buf * SF;
       const int pad = (int)(gs & 3);
       float* row0 = st + pad;
-      if (lane == 0) bulk_wait_read<1>();
+      if (lane == 0) bulk_wait_read<TABX_EMIT_NBUF - 1>();
       __syncwarp();
       {
         const int n4 = (pad + nr * D + 3) >> 2;
@@ -367,14 +372,14 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
           }
         }
       }
-      buf ^= 1;
+      buf = TABX_EMIT_NBUF == 1 ? 0 : buf ^ 1;
     }
   }
   if (glob) {
     const int64_t gs = b * (int64_t)G;
     float* st = X.stage + buf * SF;
     float* row = st + (int)(gs & 3);
-    if (lane == 0) bulk_wait_read<1>();
+    if (lane == 0) bulk_wait_read<TABX_EMIT_NBUF - 1>();
     __syncwarp();
     for (int e = lane; e < N * TABX_OWN_DIM; e += 32) {
       const int u = e / TABX_OWN_DIM;
@@ -384,7 +389,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
     fence_proxy_async();
     __syncwarp();
     flush_stage(glob, gs, G, st, lane);
-    buf ^= 1;
+    buf = TABX_EMIT_NBUF == 1 ? 0 : buf ^ 1;
   }
   if (drain) {
     if (lane == 0) bulk_wait_read<0>();
@@ -411,13 +416,18 @@ __host__ __device__ __forceinline__ int emit_stage_floats(int N, int D, int G, i
 #ifndef TABX_EMIT_BUDGET
 #define TABX_EMIT_BUDGET 3200  // stage bytes per buffer per warp (W = 1)
 #endif
+// resident CTAs per SM the register budget is cut for (W = 1: 6 CTAs of 4
+// warps = 24 warps/SM at 80 registers; W > 1: 3)
+#ifndef TABX_EMIT_MIN_BLOCKS_W1
+#define TABX_EMIT_MIN_BLOCKS_W1 6
+#endif
 #ifndef TABX_EMIT_MIN_BLOCKS
 #define TABX_EMIT_MIN_BLOCKS 3
 #endif
 // Bytes of one warp's emitter scratch (view, zone-relative table, stages).
 template <int W>
 __host__ __device__ __forceinline__ size_t emit_warp_bytes(int N, int Z, int R, int SF) {
-  return emit_view_bytes<W>(N) + emit_aux_bytes<W>(N, Z, R) + (size_t)2 * SF * sizeof(float);
+  return emit_view_bytes<W>(N) + emit_aux_bytes<W>(N, Z, R) + (size_t)TABX_EMIT_NBUF * SF * sizeof(float);
 }
 template <int W>
 __device__ __forceinline__ EmitScratch<W> emit_scratch(unsigned char* base, int N, int Z, int R) {
@@ -439,7 +449,8 @@ __device__ __forceinline__ EmitScratch<W> emit_scratch(unsigned char* base, int 
 }
 
 template <int W, int EPW, bool F16>
-__global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS)
+__global__ void __launch_bounds__(32 * EPW,
+                                  (W == 1 ? TABX_EMIT_MIN_BLOCKS_W1 : TABX_EMIT_MIN_BLOCKS))
     emit_kernel(const Params P, int R, int SF) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (is_step_mode(P.mode) && P.sync->err_index != NO_ERROR) return;

@@ -10,7 +10,7 @@ cudaError_t launch_lanes_w1(const Params& P, int sm_count, cudaStream_t stream, 
 }
 cudaError_t launch_emit_w1(const Params& P, int sm_count, cudaStream_t stream) {
   #ifndef TABX_EMIT_EPW
-#define TABX_EMIT_EPW 8
+#define TABX_EMIT_EPW 4
 #endif
   return launch_emit_t<1, TABX_EMIT_EPW>(P, sm_count, stream);
 }
