@@ -68,7 +68,7 @@ struct Sync {
   uint32_t step;
   uint32_t blocks_done;
   int32_t refresh[3];
-  int32_t pad;
+  int32_t any_pend;  // some lane awaits its auto-reset (K1 sets, K3 clears)
 };
 
 // Per-config values derived once on the device (not part of the ABI):

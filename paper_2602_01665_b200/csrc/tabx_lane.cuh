@@ -1245,7 +1245,10 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   // ---- outputs of this step (observation uses stage-8 caches, post-step state)
   const tabx_outputs& O = P.out;
   const bool resets = P.auto_reset && (lf & F_DONE);
-  if (resets) lf |= F_PEND;  // the reset kernel respawns after the emit kernel
+  if (resets) {
+    lf |= F_PEND;  // the reset kernel respawns after the emit kernel
+    if (i == 0) P.sync->any_pend = 1;
+  }
   if (valid) {
     if (O.rewards) O.rewards[u] = (float)reward_i;
     if (O.actions) O.actions[u] = act;
@@ -1362,7 +1365,10 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
     }
     __syncwarp();
   }
-  for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB) {
+  // K3 on a step where no lane finished: nothing to scan
+  const bool work = M != MODE_RESET || P.sync->any_pend != 0;
+  for (int64_t b = (int64_t)blockIdx.x * EPB + g; work && b < P.B;
+       b += (int64_t)gridDim.x * EPB) {
     if (M == MODE_RESET && !(P.st.flags[b] & F_PEND)) continue;  // env-uniform
     run_lane<W, M>(P, b, i, envs[g],
                 M == MODE_RESET ? view_base + g * view_bytes
@@ -1378,6 +1384,7 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
       const uint32_t ticket = atomicAdd(&P.sync->blocks_done, 1u);
       if (ticket == gridDim.x - 1) {
         P.sync->blocks_done = 0;
+        P.sync->any_pend = 0;
         P.sync->step = step_no + 1;
         __threadfence();
       }

@@ -2,5 +2,4 @@
 python -c "import sys; sys.path.insert(0,'.'); from paper_2602_01665_b200 import _native as n; n.lib()" || { echo "default lib broken"; exit 1; }
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
 REPS=2 bash tools/kab.sh default
-timeout 300 python bench.py --scenario c4 --no-cpu --no-e2e --rollout-envs 0 --steps 5 > gpurun_out/c4.log 2>&1
-printf "c4 " ; python -c "import json; d=json.loads(open('gpurun_out/c4.log').read().strip().splitlines()[-1]); r=d['roofline']; print(round(d['value']/1e6,3), [(k['kernel'][:6], round(k['ms_avg'],3)) for k in r['kernels']])"
+BENCH_EXTRA="--warmup 390" REPS=1 bash tools/kab.sh default
