@@ -182,10 +182,16 @@ class BatchSim:
             "reset_mask": e(B, dt=torch.bool),
         }
         self._outs = nat.TabxOutputs(*[_ptr(self._buf[k]) for k in nat.OUTPUT_FIELDS])
+        self._outs_ref = ct.byref(self._outs)
 
     def _output(self) -> BatchOutput:
+        # the buffers are persistent and BatchOutput derives final_* on
+        # access, so one view object serves every step
+        cached = getattr(self, "_out_view", None)
+        if cached is not None:
+            return cached
         b = self._buf
-        return BatchOutput(
+        self._out_view = BatchOutput(
             observations=b["observations"], global_state=b["global_state"], rewards=b["rewards"],
             action_mask=b["action_mask"], terminated=b["terminated"], truncated=b["truncated"],
             done=b["done"], dense_reward=b["dense_reward"], actions=b["actions"],
@@ -194,6 +200,7 @@ class BatchSim:
             episode_length=b["episode_length"], reset_mask=b["reset_mask"],
             _final_obs=b["final_observations"], _final_glob=b["final_global_state"],
             _auto_reset=self.auto_reset)
+        return self._out_view
 
     def _init_output(self) -> None:
         L = nat.lib()
@@ -207,8 +214,10 @@ class BatchSim:
         act_t = None
         if actions is not None:
             act_t = self._actions_tensor(actions)
-        with torch.cuda.device(self.device):
-            nat.check(L.tabx_step(self._h, _ptr(act_t), ct.byref(self._outs)), "tabx_step")
+        # (the C side selects the handle's device for its launches)
+        rc = L.tabx_step(self._h, _ptr(act_t), self._outs_ref)
+        if rc:
+            nat.check(rc, "tabx_step")
         self._keep_actions = act_t  # keep alive until the stream consumed it
         if act_t is not None and self.strict:
             self.check_errors()
