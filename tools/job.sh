@@ -1,2 +1,4 @@
 #!/bin/bash
-TABX_K0_MIN_ENVS=0 TABX_LIB=$PWD/variants/phase.so timeout 600 python tools/phase_prof.py c4_50v50 131072 5 2>&1 | tail -20
+python -c "import sys; sys.path.insert(0,'.'); from paper_2602_01665_b200 import _native as n; n.lib()" || { echo "default lib broken"; exit 1; }
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
+REPS=3 bash tools/kab.sh variants/head.so default
