@@ -40,8 +40,12 @@ class MLPPolicy(torch.nn.Module):
         self.l2 = torch.nn.Linear(hidden, (n_actions + 7) // 8 * 8)
 
     def forward(self, obs: torch.Tensor) -> torch.Tensor:
-        h = torch.relu(self.l1(obs))
-        return self.l2(h)
+        x = obs.reshape(-1, self.in_dim)
+        # bias + ReLU in the first GEMM's epilogue (cuBLASLt), no separate
+        # pass over the hidden activations
+        h = torch._addmm_activation(self.l1.bias, x, self.l1.weight.t())
+        out = torch.addmm(self.l2.bias, h, self.l2.weight.t())
+        return out.reshape(*obs.shape[:-1], out.shape[-1])
 
 
 def masked_sample(logits: torch.Tensor, mask: torch.Tensor):
