@@ -1397,13 +1397,14 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
 // the decision runs on the heuristic team's lanes only (10 of 32 in C3, 50
 // of 128 in C4) with the rest of the warp idle; here one lane is one
 // heuristic unit, over a compact per-env view staged in shared memory: for
-// W == 1 a warp packs the heuristic units of G environments, for W > 1 a warp
-// takes one environment and its lanes stride over its heuristic units.  Same inputs as K1's in-kernel call
-// (the pre-step state, the cached vis/atk rows), so the same decision; the
-// action goes to P.ctrl_act and the scripted-controller memory straight to
-// the state, where K1 reads it.  On a step that refreshes the caches (a batch
-// refill) the refresh kernel has rewritten the rows first; a step with a
-// latched action error is skipped (no mutation).
+// W == 1 a warp packs the heuristic units of G environments, for W > 1 a
+// warp takes one environment and its lanes stride over its heuristic units.
+// Same inputs as K1's in-kernel call (the pre-step state, the cached vis/atk
+// rows), so the same decision; the action goes to P.ctrl_act and the
+// scripted-controller memory straight to the state (K1 under K0 neither
+// reads nor writes it).  On a step that refreshes the caches (a batch refill)
+// the refresh kernel has rewritten the rows first; a step with a latched
+// action error is skipped (no mutation).
 template <int W>
 struct CtrlView {
   static constexpr int NT = 32 * W;
@@ -1444,19 +1445,19 @@ __global__ void __launch_bounds__(128, TABX_K0_MINB) ctrl_kernel(const Params P,
       const double mh = C->max_health[j];
       const bool act = C->active[j] != 0;
       const bool alive = (st.ubits[u] & U_ALIVE) != 0;
-      CtrlView<W>& W1 = V[gq];
-      W1.px[j] = p.x;
-      W1.py[j] = p.y;
-      W1.ch[j] = cs.x;
-      W1.sh[j] = cs.y;
-      W1.rad[j] = C->radius[j];
-      W1.mh[j] = mh;
-      W1.uf[j] = (act ? UF_ACTIVE : 0u) | (alive ? UF_ALIVE : 0u) |
+      CtrlView<W>& view = V[gq];
+      view.px[j] = p.x;
+      view.py[j] = p.y;
+      view.ch[j] = cs.x;
+      view.sh[j] = cs.y;
+      view.rad[j] = C->radius[j];
+      view.mh[j] = mh;
+      view.uf[j] = (act ? UF_ACTIVE : 0u) | (alive ? UF_ALIVE : 0u) |
                  (C->team[j] ? UF_ENEMY : 0u) | (C->kinematic[j] ? UF_KIN : 0u) |
                  (st.health[u] < mh ? UF_INJURED : 0u);
-      W1.zin[j] = st.zbits[u];
-      if (act) atomicOr(&W1.m_active[j >> 5], 1u << (j & 31));
-      if (alive) atomicOr(&W1.m_alive[j >> 5], 1u << (j & 31));
+      view.zin[j] = st.zbits[u];
+      if (act) atomicOr(&view.m_active[j >> 5], 1u << (j & 31));
+      if (alive) atomicOr(&view.m_alive[j >> 5], 1u << (j & 31));
     }
     __syncwarp();
     const int64_t b = b0 + g;
@@ -1472,29 +1473,29 @@ __global__ void __launch_bounds__(128, TABX_K0_MINB) ctrl_kernel(const Params P,
         const int64_t u = b * N + i;
         const uint8_t ub = st.ubits[u];
         if (ub & U_ALIVE) {  // free: alive, active (hlist), lane running
-          CtrlView<W>& W1 = V[g];
+          CtrlView<W>& view = V[g];
           const int team = C->team[i] ? 1 : 0;
           const double hd = st.heading[u], cd = st.cooldown[u];
           const uint32_t mask7 =
               0x1Fu | ((cd <= 0.0) ? 0x20u : 0u) | (C->enable_noop ? 0x40u : 0u);
-          const double speff = C->speed[i] * swamp_mult(C, Z, W1.zin[i], DC->swamp_m);
+          const double speff = C->speed[i] * swamp_mult(C, Z, view.zin[i], DC->swamp_m);
           const uint64_t seed = st.seed[b];
           const uint64_t t = (uint64_t)(int64_t)st.t[b];
           const double ue = uniform53(seed, t, TAG_EXPLORE, (uint64_t)i);
           const double up = uniform53(seed, t, TAG_PICK, (uint64_t)i);
 #pragma unroll
           for (int w = 0; w < W; ++w) {
-            W1.vis[i * W + w] = st.vis[u * W + w];
-            W1.atk[i * W + w] = st.atk[u * W + w];
+            view.vis[i * W + w] = st.vis[u * W + w];
+            view.atk[i * W + w] = st.atk[u * W + w];
           }
           const double2 m = st.mem_pos[u];
-          const int r = scripted_body<W>(W1, C, i, N, Z, hd, cd, speff * C->dt, mask7, ue, up,
+          const int r = scripted_body<W>(view, C, i, N, Z, hd, cd, speff * C->dt, mask7, ue, up,
                                          C->epsilon[team], C->aggressive[team], DC->bush_m, m.x,
                                          m.y, (ub & U_MEMV) != 0);
           P.ctrl_act[u] = (int8_t)(r & SA_ACT_MASK);
           if (r & SA_HAS) {
             const int tg = r >> SA_TGT_SHIFT;
-            st.mem_pos[u] = make_double2(W1.px[tg], W1.py[tg]);
+            st.mem_pos[u] = make_double2(view.px[tg], view.py[tg]);
           }
           const bool mv = (r & (SA_HAS | SA_MEMOK)) != 0;
           st.ubits[u] = (uint8_t)((ub & ~U_MEMV) | (mv ? U_MEMV : 0));
@@ -1518,8 +1519,8 @@ cudaError_t launch_ctrl_t(const Params& P, int nh, int sm_count, cudaStream_t st
   static int cached_per_sm = 0;
   int per_sm = cached_per_sm;
   if (smem != cached_smem) {
-    cudaError_t e = cudaFuncSetAttribute(ctrl_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(ctrl_kernel<W>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctrl_kernel<W>, threads, smem);
     if (e != cudaSuccess) return e;
@@ -1534,7 +1535,6 @@ cudaError_t launch_ctrl_t(const Params& P, int nh, int sm_count, cudaStream_t st
   ctrl_kernel<W><<<grid, threads, smem, stream>>>(P, G, NH);
   return cudaGetLastError();
 }
-
 
 // ------------------------------------------------------------ launchers --
 template <int W, int EPB, int M>
