@@ -8,10 +8,11 @@ cudaError_t launch_ctrl_w1(const Params& P, int nh, int sm_count, cudaStream_t s
 cudaError_t launch_lanes_w1(const Params& P, int sm_count, cudaStream_t stream, int* grid) {
   return launch_lanes_t<1, 4>(P, sm_count, stream, grid);
 }
-cudaError_t launch_emit_w1(const Params& P, int sm_count, cudaStream_t stream) {
-  #ifndef TABX_EMIT_EPW
+// observation-kernel envs (warps) per CTA at W = 1
+#ifndef TABX_EMIT_EPW
 #define TABX_EMIT_EPW 4
 #endif
+cudaError_t launch_emit_w1(const Params& P, int sm_count, cudaStream_t stream) {
   return launch_emit_t<1, TABX_EMIT_EPW>(P, sm_count, stream);
 }
 // Phase cycle counters of the instrumented build (zeros otherwise).
