@@ -1,4 +1,4 @@
 #!/bin/bash
-python tools/c5_probe.py 2>&1 | tail -4
-timeout 600 python -m pytest tests/test_gpu_parity.py -k graph_rollout -x -q 2>&1 | tail -1
-timeout 600 python -m pytest tests/test_gpu_policy.py -x -q 2>&1 | tail -1
+python -c "import sys; sys.path.insert(0,'.'); from paper_2602_01665_b200 import _native as n; n.lib()" || { echo "default lib broken"; exit 1; }
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
+REPS=3 bash tools/kab.sh variants/head.so default
