@@ -648,10 +648,13 @@ TABX_SCRIPTED_QUAL int scripted_action(const EnvSmem<W>& S, const tabx_config* _
 }
 
 // ---------------------------------------------------------------- lane ---
-template <int W, int M>
+// NF / ZF: unit / zone counts fixed at compile time (0 = P.N / P.Z): the
+// step kernel's instantiations for the common shapes, where every per-unit
+// and per-zone loop gets a constant trip count
+template <int W, int M, int NF = 0, int ZF = 0>
 __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
                          unsigned char* emit, bool refresh, uint32_t step_no) {
-  const int N = P.N, Z = P.Z;
+  const int N = NF ? NF : P.N, Z = ZF ? ZF : P.Z;
   const bool valid = i < N;
   const int64_t u = b * N + i;
   const DevState& st = P.st;
@@ -1332,7 +1335,7 @@ __host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
 // K1 (MODE_STEP / MODE_INIT / MODE_REFRESH) and K3 (MODE_RESET).
 // One kernel per mode (M): the step kernel carries no reset / emitter code,
 // which keeps its instruction footprint and register allocation to its own.
-template <int W, int EPB, int M>
+template <int W, int EPB, int M, int NF = 0, int ZF = 0>
 __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
     lane_kernel(const Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1370,7 +1373,7 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
   for (int64_t b = (int64_t)blockIdx.x * EPB + g; work && b < P.B;
        b += (int64_t)gridDim.x * EPB) {
     if (M == MODE_RESET && !(P.st.flags[b] & F_PEND)) continue;  // env-uniform
-    run_lane<W, M>(P, b, i, envs[g],
+    run_lane<W, M, NF, ZF>(P, b, i, envs[g],
                 M == MODE_RESET ? view_base + g * view_bytes
                                      : nullptr,
                 refresh, step_no);
@@ -1537,7 +1540,7 @@ cudaError_t launch_ctrl_t(const Params& P, int nh, int sm_count, cudaStream_t st
 }
 
 // ------------------------------------------------------------ launchers --
-template <int W, int EPB, int M>
+template <int W, int EPB, int M, int NF = 0, int ZF = 0>
 cudaError_t launch_lanes_m(const Params& P, int sm_count, cudaStream_t stream, int* grid_out) {
   const int threads = 32 * W * EPB;
   const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
@@ -1548,10 +1551,10 @@ cudaError_t launch_lanes_m(const Params& P, int sm_count, cudaStream_t stream, i
   static int cached_per_sm = 0;
   int per_sm = cached_per_sm;
   if (smem != cached_smem) {
-    cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB, M>,
+    cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB, M, NF, ZF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lane_kernel<W, EPB, M>, threads,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lane_kernel<W, EPB, M, NF, ZF>, threads,
                                                       smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
@@ -1563,7 +1566,7 @@ cudaError_t launch_lanes_m(const Params& P, int sm_count, cudaStream_t stream, i
   int grid = (int)(need < cap ? need : cap);
   if (grid < 1) grid = 1;
   if (grid_out) *grid_out = grid;
-  lane_kernel<W, EPB, M><<<grid, threads, smem, stream>>>(P);
+  lane_kernel<W, EPB, M, NF, ZF><<<grid, threads, smem, stream>>>(P);
   return cudaGetLastError();
 }
 
@@ -1571,7 +1574,18 @@ template <int W, int EPB>
 cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream, int* grid_out) {
   switch (P.mode) {
     case MODE_STEP: return launch_lanes_m<W, EPB, MODE_STEP>(P, sm_count, stream, grid_out);
-    case MODE_STEP_K0: return launch_lanes_m<W, EPB, MODE_STEP_K0>(P, sm_count, stream, grid_out);
+    case MODE_STEP_K0:
+      if constexpr (W == 1) {
+        // shape-specialised step kernels (C3 / C2 / C1 shapes); any other
+        // shape takes the generic one
+        if (P.N == 20 && P.Z == 6)
+          return launch_lanes_m<1, EPB, MODE_STEP_K0, 20, 6>(P, sm_count, stream, grid_out);
+        if (P.N == 20 && P.Z == 0)
+          return launch_lanes_m<1, EPB, MODE_STEP_K0, 20, 0>(P, sm_count, stream, grid_out);
+        if (P.N == 6 && P.Z == 0)
+          return launch_lanes_m<1, EPB, MODE_STEP_K0, 6, 0>(P, sm_count, stream, grid_out);
+      }
+      return launch_lanes_m<W, EPB, MODE_STEP_K0>(P, sm_count, stream, grid_out);
     case MODE_INIT: return launch_lanes_m<W, EPB, MODE_INIT>(P, sm_count, stream, grid_out);
     case MODE_REFRESH:
       return launch_lanes_m<W, EPB, MODE_REFRESH>(P, sm_count, stream, grid_out);
