@@ -398,13 +398,13 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
 }
 
 // Stage geometry: R rows per chunk within `budget` bytes per buffer.
-__host__ __device__ __forceinline__ int emit_rows(int N, int D, int budget) {
+__host__ __device__ __forceinline__ constexpr int emit_rows(int N, int D, int budget) {
   int R = budget / (4 * D);
   if (R < 1) R = 1;
   if (R > N) R = N;
   return R;
 }
-__host__ __device__ __forceinline__ int emit_stage_floats(int N, int D, int G, int R) {
+__host__ __device__ __forceinline__ constexpr int emit_stage_floats(int N, int D, int G, int R) {
   const int need = (R * D > G ? R * D : G) + 8;
   return (need + 3) & ~3;
 }
@@ -504,10 +504,81 @@ cudaError_t launch_emit_f(const Params& P, int sm_count, cudaStream_t stream) {
 
 // The bfloat16 policy feed is its own instantiation: the plain observation
 // stream carries none of its code.
+// W = 1 instantiation with the unit / zone counts (and so the row geometry)
+// fixed at compile time, for the common shapes: constant trip counts and
+// offsets, fewer live registers (no spills).  Same body as emit_kernel.
+template <int EPW, bool F16, int NF, int ZF>
+__global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS_W1)
+    emit_kernel_fixed(const Params P) {
+  constexpr int N = NF, Z = ZF;
+  constexpr int D = TABX_OWN_DIM + TABX_OTHER_DIM * (NF - 1) + TABX_ZONE_DIM * ZF;
+  constexpr int G = TABX_OWN_DIM * NF + TABX_ZONE_DIM * ZF;
+  constexpr int R = emit_rows(N, D, TABX_EMIT_BUDGET);
+  constexpr int SF = emit_stage_floats(N, D, G, R);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (is_step_mode(P.mode) && P.sync->err_index != NO_ERROR) return;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const EmitScratch<1> X =
+      emit_scratch<1>(smem_raw + (size_t)w * emit_warp_bytes<1>(N, Z, R, SF), N, Z, R);
+  const DevState& st = P.st;
+  int buf = 0;
+  for (int64_t b = (int64_t)blockIdx.x * EPW + w; b < P.B; b += (int64_t)gridDim.x * EPW) {
+    const int32_t k = st.cfg[b];
+    const tabx_config* C = P.cfgs + k;
+    const DerivedCfg* DC = P.dcfgs + k;
+    const bool pending = (st.flags[b] & F_PEND) != 0;
+    float* ob = pending ? P.out.final_observations : P.out.observations;
+    float* gb = pending ? P.out.final_global_state : P.out.global_state;
+    __nv_bfloat16* o16 = (F16 && !pending) ? (__nv_bfloat16*)P.out.observations_bf16 : nullptr;
+    if (!ob && !gb && !o16) continue;
+    load_view<1>(X, st, b, N, Z, C, DC, lane);
+    emit_lane<1, F16>(X, ob, gb, b, N, Z, D, G, R, SF, C, DC, lane, buf, false, o16,
+                      (int)P.out.observations_bf16_ld);
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
+template <int EPW, bool F16, int NF, int ZF>
+cudaError_t launch_emit_fixed(const Params& P, int sm_count, cudaStream_t stream) {
+  constexpr int D = TABX_OWN_DIM + TABX_OTHER_DIM * (NF - 1) + TABX_ZONE_DIM * ZF;
+  constexpr int G = TABX_OWN_DIM * NF + TABX_ZONE_DIM * ZF;
+  constexpr int R = emit_rows(NF, D, TABX_EMIT_BUDGET);
+  constexpr int SF = emit_stage_floats(NF, D, G, R);
+  const size_t smem = (size_t)EPW * emit_warp_bytes<1>(NF, ZF, R, SF);
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(emit_kernel_fixed<EPW, F16, NF, ZF>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int n = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, emit_kernel_fixed<EPW, F16, NF, ZF>,
+                                                      32 * EPW, smem);
+    if (e != cudaSuccess) return e;
+    per_sm = n < 1 ? 1 : n;
+  }
+  int64_t need = (P.B + EPW - 1) / EPW;
+  int64_t cap = (int64_t)sm_count * per_sm;
+  int grid = (int)(need < cap ? need : cap);
+  if (grid < 1) grid = 1;
+  emit_kernel_fixed<EPW, F16, NF, ZF><<<grid, 32 * EPW, smem, stream>>>(P);
+  return cudaGetLastError();
+}
+
+template <int W, int EPW, bool F16>
+cudaError_t launch_emit_shape(const Params& P, int sm_count, cudaStream_t stream) {
+  if constexpr (W == 1) {
+    // the C3 / C2 / C1 shapes (as the step kernel); any other: generic
+    if (P.N == 20 && P.Z == 6) return launch_emit_fixed<EPW, F16, 20, 6>(P, sm_count, stream);
+    if (P.N == 20 && P.Z == 0) return launch_emit_fixed<EPW, F16, 20, 0>(P, sm_count, stream);
+    if (P.N == 6 && P.Z == 0) return launch_emit_fixed<EPW, F16, 6, 0>(P, sm_count, stream);
+  }
+  return launch_emit_f<W, EPW, F16>(P, sm_count, stream);
+}
+
 template <int W, int EPW>
 cudaError_t launch_emit_t(const Params& P, int sm_count, cudaStream_t stream) {
-  return P.out.observations_bf16 ? launch_emit_f<W, EPW, true>(P, sm_count, stream)
-                                 : launch_emit_f<W, EPW, false>(P, sm_count, stream);
+  return P.out.observations_bf16 ? launch_emit_shape<W, EPW, true>(P, sm_count, stream)
+                                 : launch_emit_shape<W, EPW, false>(P, sm_count, stream);
 }
 
 }  // namespace tabx
