@@ -504,22 +504,23 @@ cudaError_t launch_emit_f(const Params& P, int sm_count, cudaStream_t stream) {
 
 // The bfloat16 policy feed is its own instantiation: the plain observation
 // stream carries none of its code.
-// W = 1 instantiation with the unit / zone counts (and so the row geometry)
-// fixed at compile time, for the common shapes: constant trip counts and
-// offsets, fewer live registers (no spills).  Same body as emit_kernel.
-template <int EPW, bool F16, int NF, int ZF>
-__global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS_W1)
+// Instantiations with the unit / zone counts (and so the row geometry) fixed
+// at compile time, for the common shapes: constant trip counts and offsets,
+// fewer live registers (no spills).  Same body as emit_kernel.
+template <int W, int EPW, bool F16, int NF, int ZF>
+__global__ void __launch_bounds__(32 * EPW,
+                                  (W == 1 ? TABX_EMIT_MIN_BLOCKS_W1 : TABX_EMIT_MIN_BLOCKS))
     emit_kernel_fixed(const Params P) {
   constexpr int N = NF, Z = ZF;
   constexpr int D = TABX_OWN_DIM + TABX_OTHER_DIM * (NF - 1) + TABX_ZONE_DIM * ZF;
   constexpr int G = TABX_OWN_DIM * NF + TABX_ZONE_DIM * ZF;
-  constexpr int R = emit_rows(N, D, TABX_EMIT_BUDGET);
+  constexpr int R = emit_rows(N, D, W == 1 ? TABX_EMIT_BUDGET : 8192);
   constexpr int SF = emit_stage_floats(N, D, G, R);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (is_step_mode(P.mode) && P.sync->err_index != NO_ERROR) return;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const EmitScratch<1> X =
-      emit_scratch<1>(smem_raw + (size_t)w * emit_warp_bytes<1>(N, Z, R, SF), N, Z, R);
+  const EmitScratch<W> X =
+      emit_scratch<W>(smem_raw + (size_t)w * emit_warp_bytes<W>(N, Z, R, SF), N, Z, R);
   const DevState& st = P.st;
   int buf = 0;
   for (int64_t b = (int64_t)blockIdx.x * EPW + w; b < P.B; b += (int64_t)gridDim.x * EPW) {
@@ -531,27 +532,27 @@ __global__ void __launch_bounds__(32 * EPW, TABX_EMIT_MIN_BLOCKS_W1)
     float* gb = pending ? P.out.final_global_state : P.out.global_state;
     __nv_bfloat16* o16 = (F16 && !pending) ? (__nv_bfloat16*)P.out.observations_bf16 : nullptr;
     if (!ob && !gb && !o16) continue;
-    load_view<1>(X, st, b, N, Z, C, DC, lane);
-    emit_lane<1, F16>(X, ob, gb, b, N, Z, D, G, R, SF, C, DC, lane, buf, false, o16,
+    load_view<W>(X, st, b, N, Z, C, DC, lane);
+    emit_lane<W, F16>(X, ob, gb, b, N, Z, D, G, R, SF, C, DC, lane, buf, false, o16,
                       (int)P.out.observations_bf16_ld);
   }
   if (lane == 0) bulk_wait_all();
 }
 
-template <int EPW, bool F16, int NF, int ZF>
+template <int W, int EPW, bool F16, int NF, int ZF>
 cudaError_t launch_emit_fixed(const Params& P, int sm_count, cudaStream_t stream) {
   constexpr int D = TABX_OWN_DIM + TABX_OTHER_DIM * (NF - 1) + TABX_ZONE_DIM * ZF;
   constexpr int G = TABX_OWN_DIM * NF + TABX_ZONE_DIM * ZF;
-  constexpr int R = emit_rows(NF, D, TABX_EMIT_BUDGET);
+  constexpr int R = emit_rows(NF, D, W == 1 ? TABX_EMIT_BUDGET : 8192);
   constexpr int SF = emit_stage_floats(NF, D, G, R);
-  const size_t smem = (size_t)EPW * emit_warp_bytes<1>(NF, ZF, R, SF);
+  const size_t smem = (size_t)EPW * emit_warp_bytes<W>(NF, ZF, R, SF);
   static int per_sm = 0;
   if (per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(emit_kernel_fixed<EPW, F16, NF, ZF>,
+    cudaError_t e = cudaFuncSetAttribute(emit_kernel_fixed<W, EPW, F16, NF, ZF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int n = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, emit_kernel_fixed<EPW, F16, NF, ZF>,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, emit_kernel_fixed<W, EPW, F16, NF, ZF>,
                                                       32 * EPW, smem);
     if (e != cudaSuccess) return e;
     per_sm = n < 1 ? 1 : n;
@@ -560,17 +561,21 @@ cudaError_t launch_emit_fixed(const Params& P, int sm_count, cudaStream_t stream
   int64_t cap = (int64_t)sm_count * per_sm;
   int grid = (int)(need < cap ? need : cap);
   if (grid < 1) grid = 1;
-  emit_kernel_fixed<EPW, F16, NF, ZF><<<grid, 32 * EPW, smem, stream>>>(P);
+  emit_kernel_fixed<W, EPW, F16, NF, ZF><<<grid, 32 * EPW, smem, stream>>>(P);
   return cudaGetLastError();
 }
 
 template <int W, int EPW, bool F16>
 cudaError_t launch_emit_shape(const Params& P, int sm_count, cudaStream_t stream) {
+  // the C3 / C2 / C1 / C4 shapes (as the step kernel); any other: generic
   if constexpr (W == 1) {
-    // the C3 / C2 / C1 shapes (as the step kernel); any other: generic
-    if (P.N == 20 && P.Z == 6) return launch_emit_fixed<EPW, F16, 20, 6>(P, sm_count, stream);
-    if (P.N == 20 && P.Z == 0) return launch_emit_fixed<EPW, F16, 20, 0>(P, sm_count, stream);
-    if (P.N == 6 && P.Z == 0) return launch_emit_fixed<EPW, F16, 6, 0>(P, sm_count, stream);
+    if (P.N == 20 && P.Z == 6) return launch_emit_fixed<1, EPW, F16, 20, 6>(P, sm_count, stream);
+    if (P.N == 20 && P.Z == 0) return launch_emit_fixed<1, EPW, F16, 20, 0>(P, sm_count, stream);
+    if (P.N == 6 && P.Z == 0) return launch_emit_fixed<1, EPW, F16, 6, 0>(P, sm_count, stream);
+  }
+  if constexpr (W == 4) {
+    if (P.N == 100 && P.Z == 0)
+      return launch_emit_fixed<4, EPW, F16, 100, 0>(P, sm_count, stream);
   }
   return launch_emit_f<W, EPW, F16>(P, sm_count, stream);
 }

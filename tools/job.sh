@@ -1,4 +1,11 @@
 #!/bin/bash
 python -c "import sys; sys.path.insert(0,'.'); from paper_2602_01665_b200 import _native as n; n.lib()" || { echo "default lib broken"; exit 1; }
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pt.log 2>&1; tail -1 gpurun_out/pt.log
-REPS=3 bash tools/kab.sh variants/head.so default
+for r in 1 2; do
+for lib in variants/head.so default; do
+  if [ "$lib" = default ]; then unset TABX_LIB; else export TABX_LIB=$PWD/$lib; fi
+  timeout 300 python bench.py --scenario c4 --no-cpu --no-e2e --rollout-envs 0 --steps 5 > gpurun_out/s.log 2>&1
+  printf "c4 %-18s " "$lib"; python -c "import json; d=json.loads(open('gpurun_out/s.log').read().strip().splitlines()[-1]); r=d['roofline']; print(round(d['value']/1e6,3), [(k['kernel'][:6], round(k['ms_avg'],3)) for k in r['kernels']])"
+done
+done
+REPS=1 bash tools/kab.sh default
