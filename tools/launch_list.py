@@ -8,12 +8,13 @@ The ncu command is the recipe's launch pass with DRAM bytes added:
         --clock-control none --csv python bench.py --steps 2 --warmup 1 --no-cpu \
         --no-e2e --rollout-envs 0 --envs 65536
 The traffic file records the DRAM bytes per env-step of one whole step (the
-controller-pass / step kernel launch given through the reset kernel that
-ends the step), which bench.py reports as ``roofline.traffic``.
+controller-pass / step kernel launch given through the reset kernel,
+lane_kernel<W, EPB, 3, ...>, that ends the step), which bench.py reports as ``roofline.traffic``.
 """
 from __future__ import annotations
 
 import csv
+import re
 import io
 import json
 import sys
@@ -51,7 +52,7 @@ def main(argv) -> int:
     step = []
     for k in sorted(x for x in data if x >= first):
         step.append(data[k])
-        if data[k]["kernel"].rstrip().endswith(", 3>"):
+        if re.match(r"(void )?lane_kernel<\d+, \d+, 3[,>]", data[k]["kernel"].strip()):
             break
     total = sum(d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
                 for d in step)
