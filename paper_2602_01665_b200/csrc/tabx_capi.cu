@@ -63,6 +63,7 @@ struct tabx_handle {
   // heuristic units per env over the config table (recounted when it changes)
   int8_t* ctrl_act = nullptr;
   int cfg_version = 0, ctrl_version = -1, ctrl_nh = 0;
+  int generic_shapes = 0;  // TABX_GENERIC_SHAPES=1: skip the shape-specialised kernels
   std::vector<tabx_config> cfg_host;  // host mirror of the table rows
   std::vector<char> cfg_host_ok;       // 0: row written on the device (tabx_levels)
   int cfg_cap = TABX_MAX_CONFIGS;
@@ -150,6 +151,7 @@ static Params make_params(tabx_handle* h, int mode, const int64_t* actions,
   P.auto_reset = h->auto_reset;
   P.mode = mode;
   P.ctrl_act = nullptr;
+  P.generic_shapes = h->generic_shapes;
   return P;
 }
 
@@ -326,6 +328,8 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   const int64_t k0_envs = k0_min ? atoll(k0_min) : 4096;
   if (B >= k0_envs && !(no_k0 && no_k0[0] == '1'))
     h->ctrl_act = (int8_t*)(a + o_ctl);
+  const char* gen = getenv("TABX_GENERIC_SHAPES");
+  h->generic_shapes = (gen && gen[0] == '1') ? 1 : 0;
 
   int rc = TABX_OK;
   for (int k = 0; k < n_configs; ++k) {

@@ -109,6 +109,7 @@ struct Params {
   // K0 (heuristic controller pass): its action per unit, or nullptr
   // when K1 runs the controller itself
   int8_t* ctrl_act;
+  int generic_shapes;  // 1: no shape-specialised kernel instantiations
 };
 
 __device__ __noinline__ static bool zone_exact(double ex, double ey, double ax, double ay) {

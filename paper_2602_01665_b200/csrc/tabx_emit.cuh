@@ -568,6 +568,7 @@ cudaError_t launch_emit_fixed(const Params& P, int sm_count, cudaStream_t stream
 template <int W, int EPW, bool F16>
 cudaError_t launch_emit_shape(const Params& P, int sm_count, cudaStream_t stream) {
   // the C3 / C2 / C1 / C4 shapes (as the step kernel); any other: generic
+  if (P.generic_shapes) return launch_emit_f<W, EPW, F16>(P, sm_count, stream);
   if constexpr (W == 1) {
     if (P.N == 20 && P.Z == 6) return launch_emit_fixed<1, EPW, F16, 20, 6>(P, sm_count, stream);
     if (P.N == 20 && P.Z == 0) return launch_emit_fixed<1, EPW, F16, 20, 0>(P, sm_count, stream);

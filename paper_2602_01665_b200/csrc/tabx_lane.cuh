@@ -1575,18 +1575,18 @@ cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream, i
   switch (P.mode) {
     case MODE_STEP: return launch_lanes_m<W, EPB, MODE_STEP>(P, sm_count, stream, grid_out);
     case MODE_STEP_K0:
+      // shape-specialised step kernels (C3 / C2 / C1 / C4 shapes); any other
+      // shape, or TABX_GENERIC_SHAPES=1, takes the generic one
       if constexpr (W == 1) {
-        // shape-specialised step kernels (C3 / C2 / C1 shapes, C4 below); any
-        // other shape takes the generic one
-        if (P.N == 20 && P.Z == 6)
+        if (!P.generic_shapes && P.N == 20 && P.Z == 6)
           return launch_lanes_m<1, EPB, MODE_STEP_K0, 20, 6>(P, sm_count, stream, grid_out);
-        if (P.N == 20 && P.Z == 0)
+        if (!P.generic_shapes && P.N == 20 && P.Z == 0)
           return launch_lanes_m<1, EPB, MODE_STEP_K0, 20, 0>(P, sm_count, stream, grid_out);
-        if (P.N == 6 && P.Z == 0)
+        if (!P.generic_shapes && P.N == 6 && P.Z == 0)
           return launch_lanes_m<1, EPB, MODE_STEP_K0, 6, 0>(P, sm_count, stream, grid_out);
       }
-      if constexpr (W == 4) {  // the C4 shape
-        if (P.N == 100 && P.Z == 0)
+      if constexpr (W == 4) {
+        if (!P.generic_shapes && P.N == 100 && P.Z == 0)
           return launch_lanes_m<4, EPB, MODE_STEP_K0, 100, 0>(P, sm_count, stream, grid_out);
       }
       return launch_lanes_m<W, EPB, MODE_STEP_K0>(P, sm_count, stream, grid_out);

@@ -466,3 +466,26 @@ def test_controller_pass_graph_after_config_growth():
             bad.append(f"graph t={t}: observations differ")
         assert not bad, "\n".join(bad[:10])
     gpu.close()
+
+
+@pytest.mark.parametrize("scen,B", [("c3_10v10_terrain", 8192), ("c2_10v10", 8192),
+                                    ("c4_50v50", 1024)])
+def test_shape_specialised_kernels_equal_generic(scen, B, monkeypatch):
+    """The step and observation kernels compiled for a fixed (N, Z) and the
+    generic ones (TABX_GENERIC_SHAPES=1, read when the batch is created) give
+    identical observations, rewards and state step for step."""
+    sc = builtin_scenario(scen)
+    seeds = np.arange(B, dtype=np.uint64) + 11
+    sims = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("TABX_GENERIC_SHAPES", flag)
+        sims.append(BatchSim([sc] * B, seeds, auto_reset=True, device="cuda:0",
+                             interactions=False))
+    for t in range(30):
+        outs = [s.step(None) for s in sims]
+        assert torch.equal(outs[0].observations, outs[1].observations), t
+        assert torch.equal(outs[0].global_state, outs[1].global_state), t
+        assert torch.equal(outs[0].rewards, outs[1].rewards), t
+    s0, s1 = (s.export_state() for s in sims)
+    for k in ("pos", "health", "heading", "alive", "mem_pos", "vis", "atk"):
+        assert torch.equal(s0[k], s1[k]), k
