@@ -183,6 +183,7 @@ class BatchSim:
         }
         self._outs = nat.TabxOutputs(*[_ptr(self._buf[k]) for k in nat.OUTPUT_FIELDS])
         self._outs_ref = ct.byref(self._outs)
+        self._step_fn = nat.lib().tabx_step
 
     def _output(self) -> BatchOutput:
         # the buffers are persistent and BatchOutput derives final_* on
@@ -210,12 +211,11 @@ class BatchSim:
 
     # ---------------------------------------------------------------- api --
     def step(self, actions=None) -> BatchOutput:
-        L = nat.lib()
         act_t = None
         if actions is not None:
             act_t = self._actions_tensor(actions)
         # (the C side selects the handle's device for its launches)
-        rc = L.tabx_step(self._h, _ptr(act_t), self._outs_ref)
+        rc = self._step_fn(self._h, _ptr(act_t), self._outs_ref)
         if rc:
             nat.check(rc, "tabx_step")
         self._keep_actions = act_t  # keep alive until the stream consumed it
