@@ -1,2 +1,2 @@
 #!/bin/bash
-timeout 600 python tools/soak_probe.py 2>&1 | tail -4
+for w in 5 100 200 390; do printf "warmup $w: "; BENCH_EXTRA="--warmup $w" REPS=1 bash tools/kab.sh default; done
