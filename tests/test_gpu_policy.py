@@ -87,3 +87,31 @@ def test_bf16_policy_feed_equals_packed_observations():
         resets += int(ro.sim._buf["reset_mask"].sum())
     assert resets > 0
     ro.close()
+
+
+def test_bf16_policy_feed_rejects_bad_rows():
+    """The bf16 feed must be 16-byte aligned with a row stride that is a
+    multiple of 8 and at least obs_dim (tabx.h): tabx_step refuses others
+    with TABX_E_ALIGNMENT before launching anything."""
+    import numpy as np
+
+    from paper_2602_01665_b200.scenario import builtin_scenario
+    from paper_2602_01665_b200.sim import BatchSim
+    sc = builtin_scenario("c1_3v3")
+    sim = BatchSim([sc] * 8, np.arange(8, dtype=np.uint64), auto_reset=True, device=0)
+    D = sim.obs_dim
+    Dp = (D + 7) // 8 * 8
+    buf = torch.zeros(8 * sim.n_units * Dp + 16, dtype=torch.bfloat16, device="cuda")
+    L = nat.lib()
+    for ptr, ld in ((buf.data_ptr() + 2, Dp), (buf.data_ptr(), Dp + 4), (buf.data_ptr(), Dp - 8)):
+        outs = nat.TabxOutputs.from_buffer_copy(sim._outs)
+        outs.observations_bf16 = ptr
+        outs.observations_bf16_ld = ld
+        rc = L.tabx_step(sim.handle, None, ct.byref(outs))
+        assert rc == nat.E_ALIGNMENT, (ptr - buf.data_ptr(), ld, rc)
+    outs = nat.TabxOutputs.from_buffer_copy(sim._outs)
+    outs.observations_bf16 = buf.data_ptr()
+    outs.observations_bf16_ld = Dp
+    nat.check(L.tabx_step(sim.handle, None, ct.byref(outs)), "tabx_step")
+    torch.cuda.synchronize()
+    sim.close()
