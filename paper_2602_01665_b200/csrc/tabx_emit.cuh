@@ -21,11 +21,18 @@ namespace tabx {
 // Per-warp view of one environment, laid out in dynamic shared memory for
 // the batch's N units: positions, the 15 own features (16-float rows), the
 // N-bit visibility / attackable rows, unit flags.
+// floats per unit row of the view's own-feature table (15 used): a multiple
+// of 4 keeps the rows 16-byte aligned for the float4 reads of the pair
+// blocks, and 20 (not 16) spreads eight consecutive rows over distinct bank
+// groups (fewer shared-memory bank conflicts in those reads)
+#ifndef TABX_OWN_STRIDE
+#define TABX_OWN_STRIDE 20
+#endif
 template <int W>
 struct EmitEnv {
   double* px;
   double* py;
-  float (*own)[16];
+  float (*own)[TABX_OWN_STRIDE];
   uint32_t* vis;
   uint32_t* atk;
   uint32_t* flags;  // bit0 active, bit1 enemy
@@ -44,7 +51,8 @@ struct EmitScratch {
 __host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 template <int W>
 __host__ __device__ __forceinline__ size_t emit_view_bytes(int N) {
-  return align16((size_t)16 * N) + (size_t)64 * N + align16((size_t)4 * N * (2 * W + 1));
+  return align16((size_t)16 * N) + (size_t)4 * TABX_OWN_STRIDE * N +
+         align16((size_t)4 * N * (2 * W + 1));
 }
 template <int W>
 __host__ __device__ __forceinline__ size_t emit_aux_bytes(int N, int Z, int R) {
@@ -436,8 +444,8 @@ __device__ __forceinline__ EmitScratch<W> emit_scratch(unsigned char* base, int 
   X.E.px = reinterpret_cast<double*>(p);
   X.E.py = X.E.px + N;
   p += align16((size_t)16 * N);
-  X.E.own = reinterpret_cast<float(*)[16]>(p);
-  p += (size_t)64 * N;
+  X.E.own = reinterpret_cast<float(*)[TABX_OWN_STRIDE]>(p);
+  p += (size_t)4 * TABX_OWN_STRIDE * N;
   X.E.vis = reinterpret_cast<uint32_t*>(p);
   X.E.atk = X.E.vis + N * W;
   X.E.flags = X.E.atk + N * W;
