@@ -15,10 +15,15 @@ rollout.py:360-366); auto-reset on; episodes truncate at t=400.
   HBM, CUDA-event timed over K steps (max over ranks).  Each step writes
   ~8.1 GB of observations, so every timed step streams far more than L2.
 * ``e2e``: the same metric through the trainer API (``bindings.HostStepper``
-  over ``bindings.step``) with host buffers: int64 actions copied from pinned
-  host memory every step (ally team external), rewards + terminated +
-  truncated copied back every step; the copies run on a copy stream and
-  overlap the neighbouring steps' kernels.
+  over ``bindings.step``) with host buffers, for the same K steps: int64
+  actions copied from pinned host memory every step (ally team external),
+  rewards + terminated + truncated copied back every step; the copies run on
+  copy streams and overlap the neighbouring steps' kernels.  Observations
+  and masks stay on the device; ``host_obs_e2e`` prices copying them out.
+* ``c1`` / ``c2`` / ``c4``: the other BASELINE configs (value, roofline, e2e)
+  measured the same way in the same run; ``c3_episode``: a whole episode
+  (t = 1..410 from the start, across the lockstep t = 400 auto-reset);
+  ``reconfig``: the reference's reconfiguration-latency protocol.
 * ``roofline``: the step kernel's algorithmic HBM bytes (SURVEY.md §8(d):
   4·N·obs_dim + 4·gdim + 4N + 7N + 3 + 8N + 2·(89N+40) per env-step) per
   launch ÷ its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs.
@@ -210,95 +215,164 @@ def run_reference_arm(args) -> int:
     return 0
 
 
-def run_gpu_arm(args) -> int:
-    import numpy as np
-    import torch
-    import torch.distributed as dist
+class Ctx:
+    """Rank / device plumbing shared by the measurements."""
 
-    from paper_2602_01665_b200 import bindings, shard
-    from paper_2602_01665_b200.rng import lane_seeds
-    from paper_2602_01665_b200.scenario import builtin_scenario, save_scenario
-    from paper_2602_01665_b200.sim import BatchSim
+    def __init__(self):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.rank, self.world, self.local = dist_env()
+        torch.cuda.set_device(self.local)
+        self.dev = torch.device("cuda", self.local)
+        if self.world > 1:
+            dist.init_process_group("nccl", device_id=self.dev)
+        self.stream = torch.cuda.current_stream(self.dev)
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    # weak scaling: every GPU steps its own full batch (lanes are independent;
-    # rank g owns the global lanes [g*per, (g+1)*per) with their global seeds)
-    per = args.envs or DEFAULT_ENVS[args.scenario]
-    total = per * world
-    first, _ = shard.shard_range(total, world, rank)
-    base = builtin_scenario(SCENARIOS[args.scenario])
-    sc = base.scripted()
-    N, Z = sc.max_units, sc.max_zones
-    seeds = lane_seeds(args.seed, per, first)
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
-    # ---------------- device-resident throughput (value + roofline)
-    sim = BatchSim([sc] * per, seeds, auto_reset=True, device=dev, interactions=False)
-    stream = torch.cuda.current_stream(dev)
-    for _ in range(args.warmup):
+    def event(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+
+def launches_per_step(per: int) -> int:
+    # K1, K2, K3 per step, plus the refresh check and K0 (the
+    # heuristic-controller pass) from 4,096 lanes on unless disabled
+    k0 = per >= int(os.environ.get("TABX_K0_MIN_ENVS", 4096)) and os.environ.get("TABX_NO_K0") != "1"
+    return 3 + (2 if k0 else 0)
+
+
+def measure_device(cx: Ctx, key: str, per: int, steps: int, warmup: int, seed: int,
+                   profile: bool = True, stats: bool = False) -> dict:
+    """value (+ roofline): K steps of a resident batch, CUDA-event timed."""
+    from paper_2602_01665_b200 import shard
+    from paper_2602_01665_b200.rng import lane_seeds
+    from paper_2602_01665_b200.scenario import builtin_scenario
+    from paper_2602_01665_b200.sim import BatchSim
+
+    torch = cx.torch
+    total = per * cx.world
+    first, _ = shard.shard_range(total, cx.world, cx.rank)
+    sc = builtin_scenario(SCENARIOS[key]).scripted()
+    N, Z = sc.max_units, sc.max_zones
+    sim = BatchSim([sc] * per, lane_seeds(seed, per, first), auto_reset=True, device=cx.dev,
+                   interactions=False, final_observations=(key != "c4"))
+    for _ in range(warmup):
         sim.step(None)
-    barrier()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        t0.record(stream)
-        for k in range(args.steps):
+    cx.barrier()
+    t0, t1 = cx.event(), cx.event()
+    with ClockSampler(cx.local) as clk:
+        t0.record(cx.stream)
+        for _ in range(steps):
             sim.step(None)
-        t1.record(stream)
-        barrier()
-    elapsed_ms = max_over_ranks(t0.elapsed_time(t1))
-    # per-kernel times (roofline) from a second pass of the same length with
-    # CUDA events around every kernel, so their host cost stays out of `value`
-    sim.set_profiling(True)
-    for k in range(args.steps):
-        starts[k].record(stream)
-        sim.step(None)
-        ends[k].record(stream)
-    barrier()
-    kprof = sim.kernel_profile()
-    sim.set_profiling(False)
-    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    value = total * args.steps / (elapsed_ms / 1000.0)
-    # the one collective: per-window episode statistics, NCCL all-reduce over NVLink
-    stats = shard.reduce_episode_stats(sim.episode_stats(), device=dev)
-    stats["summary"] = shard.summarize(stats)
+        t1.record(cx.stream)
+        cx.barrier()
+    elapsed_ms = cx.max_over_ranks(t0.elapsed_time(t1))
+    out = {"value": total * steps / (elapsed_ms / 1000.0), "unit": "env-steps/s",
+           "ms_per_step": elapsed_ms / steps, "steps": steps, "warmup": warmup,
+           "agent_steps_per_s": total * steps / (elapsed_ms / 1000.0) * len(sc.units),
+           "envs": total, "envs_per_gpu": per, "n_units": N, "n_zones": Z,
+           "clocks": clk.summary(), "gpu_launches": launches_per_step(per) * steps}
+    if profile:
+        # per-kernel times (roofline) from a second pass of the same length with
+        # CUDA events around every kernel, so their host cost stays out of `value`
+        starts = [cx.event() for _ in range(steps)]
+        ends = [cx.event() for _ in range(steps)]
+        sim.set_profiling(True)
+        for k in range(steps):
+            starts[k].record(cx.stream)
+            sim.step(None)
+            ends[k].record(cx.stream)
+        cx.barrier()
+        kprof = sim.kernel_profile()
+        sim.set_profiling(False)
+        kern_ms = statistics.mean(s.elapsed_time(e) for s, e in zip(starts, ends))
+        out["roofline"] = roofline(key, N, Z, per, kern_ms, kprof)
+    if stats:
+        # the one collective: per-window episode statistics, NCCL all-reduce over NVLink
+        st = shard.reduce_episode_stats(sim.episode_stats(), device=cx.dev)
+        st["summary"] = shard.summarize(st)
+        out["episode_stats"] = st
     sim.close()
     del sim
     torch.cuda.empty_cache()
+    return out
 
-    # ---------------- end-to-end through the trainer API with host buffers
-    e2e_steps = 0 if args.no_e2e else max(3, min(args.steps, args.e2e_steps))
+
+def roofline(key: str, N: int, Z: int, per: int, kern_ms: float, kprof: dict) -> dict:
+    peaks = load_peaks()
+    peak = peaks.get("hbm_gbs", 6547.5)
+    bytes_per = algorithmic_bytes(N, Z)
+    achieved = bytes_per * per / (kern_ms / 1000.0) / 1e9
+    D, G = sim_dims(N, Z)
+    obs_bytes = 4 * N * D + 4 * G + 57 * N + 5  # writes + the per-unit view it reads
+    step_bytes = bytes_per - (4 * N * D + 4 * G)
+    kernels = []
+    for name, ms, nbytes in (("step_kernels (K0 heuristic-controller pass + K1 actions..rewards, "
+                              "caches, state)", kprof["step_kernel_ms"], step_bytes),
+                             ("obs_kernel (K2: observation + global-state stream, TMA)",
+                              kprof["obs_kernel_ms"], obs_bytes),
+                             ("reset_kernel (K3: deferred auto-resets)",
+                              kprof["reset_kernel_ms"], None)):
+        ent = {"kernel": name, "ms_avg": ms}
+        if nbytes and ms > 0:
+            gbs = nbytes * per / (ms / 1000.0) / 1e9
+            ent.update({"bytes_per_env_step": nbytes, "achieved_gbs": gbs, "frac": gbs / peak})
+        if "obs_kernel" in name and ms > 0:
+            strict = (4 * N * D + 4 * G) * per / (ms / 1000.0) / 1e9
+            ent["frac_obs_bytes_only"] = strict / peak
+        kernels.append(ent)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{key}.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("bytes_per_env_step", 0) * per or None
+    return {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic, "bytes_per_env_step": bytes_per,
+            "kernel_ms_avg": kern_ms,
+            "scope": "one step = controller pass + step kernel + observation kernel + reset "
+                     "kernel (SURVEY.md 8(d) bytes per env-step x envs / step time)",
+            "kernels": kernels,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks
+            else "fallback (B200_PROFILING.md)"}
+
+
+def measure_e2e(cx: Ctx, key: str, per: int, steps: int, warmup: int, seed: int) -> dict:
+    """The metric through the trainer API with host buffers (bindings.HostStepper)."""
+    import numpy as np
+
+    from paper_2602_01665_b200 import bindings, shard
+    from paper_2602_01665_b200.scenario import builtin_scenario, save_scenario
+
+    torch = cx.torch
+    total = per * cx.world
+    first, _ = shard.shard_range(total, cx.world, cx.rank)
+    base = builtin_scenario(SCENARIOS[key])
+    N = base.max_units
     doc = save_scenario(base).encode()  # ally external, enemy heuristic-medium
-    h = bindings.make_batch(doc, per, args.seed, device=dev, first_lane=first,
-                            interactions=False, final_observations=True)
-    gen = np.random.default_rng(1234 + rank)
+    h = bindings.make_batch(doc, per, seed, device=cx.dev, first_lane=first,
+                            interactions=False, final_observations=(key != "c4"))
+    gen = np.random.default_rng(1234 + cx.rank)
     pinned = [torch.from_numpy(gen.integers(0, 5, size=(per, N), dtype=np.int64)).pin_memory()
               for _ in range(4)]  # moves/rotate: always legal, no host mask round trip
     # bindings.HostStepper: every step uploads its host actions and downloads
-    # its rewards / terminated / truncated through pinned double buffers on a
-    # copy stream, overlapping the neighbouring steps' kernels; the host
+    # its rewards / terminated / truncated through pinned double buffers on
+    # copy streams, overlapping the neighbouring steps' kernels; the host
     # consumes step k-1's results while step k runs
     stepper = bindings.HostStepper(h)
     host_sum = 0.0
 
-    def e2e_run(n):
+    def run(n):
         nonlocal host_sum
         prev = None
         for k in range(n):
@@ -311,38 +385,134 @@ def run_gpu_arm(args) -> int:
             rew_h, term_h, trunc_h = stepper.result(prev)
             host_sum += float(rew_h[0, 0])
 
-    e2e_run(args.warmup if e2e_steps else 0)
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    run(warmup)
+    cx.barrier()
+    e0, e1 = cx.event(), cx.event()
     w0 = time.perf_counter()
-    e0.record(stream)
-    e2e_run(e2e_steps)
-    e1.record(stream)
-    barrier()
+    e0.record(cx.stream)
+    run(steps)
+    e1.record(cx.stream)
+    cx.barrier()
     wall = time.perf_counter() - w0
-    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), 1000.0 * wall))
-    e2e_value = total * e2e_steps / (e2e_ms / 1000.0) if e2e_steps else None
+    ms = cx.max_over_ranks(max(e0.elapsed_time(e1), 1000.0 * wall))
     h.sim.close()
+    del h, stepper
+    torch.cuda.empty_cache()
+    return {"value": total * steps / (ms / 1000.0), "unit": "env-steps/s",
+            "h2d_bytes_per_step": per * N * 8, "d2h_bytes_per_step": per * N * 4 + 2 * per,
+            "steps": steps}
+
+
+def measure_host_obs(cx: Ctx, key: str, per: int, steps: int, seed: int) -> dict:
+    """What a host-side consumer of the reference's numpy outputs pays: every
+    step's float32 observations copied to pinned host memory (PCIe bound)."""
+    from paper_2602_01665_b200 import bindings, shard
+    from paper_2602_01665_b200.scenario import builtin_scenario, save_scenario
+
+    torch = cx.torch
+    total = per * cx.world
+    first, _ = shard.shard_range(total, cx.world, cx.rank)
+    base = builtin_scenario(SCENARIOS[key])
+    h = bindings.make_batch(save_scenario(base.scripted()).encode(), per, seed, device=cx.dev,
+                            first_lane=first, interactions=False, final_observations=False)
+    obs = h.sim.last.observations
+    host = torch.empty(obs.shape, dtype=obs.dtype).pin_memory()
+    mask_host = torch.empty(h.sim.last.action_mask.shape, dtype=torch.bool).pin_memory()
+    bindings.step(h, None)
+    cx.barrier()
+    e0, e1 = cx.event(), cx.event()
+    e0.record(cx.stream)
+    for _ in range(steps):
+        out = bindings.step(h, None)
+        host.copy_(out[0], non_blocking=True)
+        mask_host.copy_(out[5], non_blocking=True)
+    e1.record(cx.stream)
+    cx.barrier()
+    ms = cx.max_over_ranks(e0.elapsed_time(e1))
+    h.sim.close()
+    del h, host, mask_host
+    torch.cuda.empty_cache()
+    return {"value": total * steps / (ms / 1000.0), "unit": "env-steps/s", "steps": steps,
+            "d2h_bytes_per_step": per * (obs.shape[1] * obs.shape[2] * 4 + obs.shape[1] * 7),
+            "note": "bindings.step + observations and action mask copied to pinned host "
+                    "memory every step (the reference's step returns numpy arrays); bound by "
+                    "the PCIe device-to-host link"}
+
+
+def measure_reconfig(cx: Ctx, batches=(8, 262144)) -> dict:
+    from paper_2602_01665_b200.reconfig import reconfiguration_latency
+    from paper_2602_01665_b200.scenario import builtin_scenario
+
+    out = {"protocol": "rollout.py:422-448 (100 distinct scenarios through reset_env(i % "
+                       "lanes, config_i, seed=i), a step after each); gate: worst < 10 ms "
+                       "(pkg/tests/test_acceptance.py:425-433); times to completion (host call "
+                       "+ stream synchronise)"}
+    for b in batches:
+        r = reconfiguration_latency(builtin_scenario(SCENARIOS["c3"]), count=100, batch=b,
+                                    device=cx.local)
+        out[f"batch_{b}"] = {"worst_ms": 1000 * max(r["times"]),
+                             "mean_ms": 1000 * statistics.mean(r["times"]),
+                             "host_call_mean_ms": 1000 * statistics.mean(r["host_times"]),
+                             "config_rows": r["config_rows"]}
+        cx.torch.cuda.empty_cache()
+    return out
+
+
+def run_gpu_arm(args) -> int:
+    cx = Ctx()
+    key = args.scenario
+    per = args.envs or DEFAULT_ENVS[key]
+    total = per * cx.world
+    from paper_2602_01665_b200.scenario import builtin_scenario
+    sc = builtin_scenario(SCENARIOS[key]).scripted()
+    N, Z = sc.max_units, sc.max_zones
+
+    # ---------------- headline: device-resident throughput (value + roofline)
+    head = measure_device(cx, key, per, args.steps, args.warmup, args.seed, stats=True)
+    # ---------------- end-to-end through the trainer API with host buffers
+    e2e = None if args.no_e2e else measure_e2e(cx, key, per, args.steps, args.warmup, args.seed)
+
+    # ---------------- the other BASELINE configs, each timed the same way
+    extras = {}
+    for k in [c for c in args.configs.split(",") if c and c != key]:
+        p = DEFAULT_ENVS[k]
+        m = measure_device(cx, k, p, args.steps, args.warmup, args.seed)
+        if not args.no_e2e:
+            m["e2e"] = measure_e2e(cx, k, p, args.steps, args.warmup, args.seed)
+        m["workload"] = WORKLOAD[k]
+        extras[k] = m
+    # ---------------- a whole episode of the headline config: t = 1..K,
+    # across the lockstep truncation at t = 400 (every lane auto-resets, the
+    # next step refreshes every cache)
+    episode = None
+    if args.episode_steps > 0:
+        episode = measure_device(cx, key, per, args.episode_steps, 0, args.seed, profile=False)
+        episode["window"] = (f"t = 1..{args.episode_steps} from the episode start (no warm-up), "
+                             "including the lockstep t = 400 truncation + auto-reset")
+    host_obs = None
+    if args.host_obs_steps > 0:
+        host_obs = measure_host_obs(cx, key, per, args.host_obs_steps, args.seed)
+    reconfig = measure_reconfig(cx) if args.reconfig and cx.world == 1 else None
 
     # ---------------- C5: full rollout loop (policy + step + auto-reset), CUDA graph
     c5 = None
     if args.rollout_envs > 0:
+        from paper_2602_01665_b200 import shard
         from paper_2602_01665_b200.rollout import Rollout
-        r_total = args.rollout_envs * world
-        r_first, r_per = shard.shard_range(r_total, world, rank)
-        ro = Rollout(base, r_per, horizon=args.horizon, policy=args.policy, device=local,
+        base = builtin_scenario(SCENARIOS[key])
+        r_total = args.rollout_envs * cx.world
+        r_first, r_per = shard.shard_range(r_total, cx.world, cx.rank)
+        ro = Rollout(base, r_per, horizon=args.horizon, policy=args.policy, device=cx.local,
                      seed=args.seed, first_lane=r_first)
         ro.run()  # capture + first horizon
-        barrier()
-        r0 = torch.cuda.Event(enable_timing=True)
-        r1 = torch.cuda.Event(enable_timing=True)
-        r0.record(stream)
+        cx.barrier()
+        r0, r1 = cx.event(), cx.event()
+        r0.record(cx.stream)
         for _ in range(args.rollout_iters):
             ro.run()
-        r1.record(stream)
-        barrier()
-        r_ms = max_over_ranks(r0.elapsed_time(r1))
+        r1.record(cx.stream)
+        cx.barrier()
+        r_ms = cx.max_over_ranks(r0.elapsed_time(r1))
         c5 = {"value": r_total * args.horizon * args.rollout_iters / (r_ms / 1000.0),
               "unit": "env-steps/s", "envs": r_total, "horizon": args.horizon,
               "policy": args.policy, "iterations": args.rollout_iters,
@@ -352,84 +522,59 @@ def run_gpu_arm(args) -> int:
                       "[T+1,B,N,D] horizon buffer"}
         ro.close()
         del ro
-        torch.cuda.empty_cache()
+        cx.torch.cuda.empty_cache()
 
     # ---------------- CPU baseline (rank 0, N=1 only)
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        r = cpu_reference(args.scenario, args.cpu_envs, args.cpu_steps, 1)
+    if cx.rank == 0 and cx.world == 1 and not args.no_cpu:
+        r = cpu_reference(key, args.cpu_envs, args.cpu_steps, 1)
         cpu = {"value": r["env_steps_per_s"], "unit": "env-steps/s", "cores": 1, "kind": "port",
                "sample": f"{r['envs']} envs x {r['steps']} steps (+1 warm-up), "
                          f"oracle/tabx_oracle.py numpy {r['numpy']}, {r['seconds']:.1f} s"}
 
-    if rank == 0:
-        peaks = load_peaks()
-        peak = peaks.get("hbm_gbs", 6451.2)
-        bytes_per = algorithmic_bytes(N, Z)
-        kern_avg = statistics.mean(kern_ms)
-        achieved = bytes_per * per / (kern_avg / 1000.0) / 1e9
+    if cx.rank == 0:
         D, G = sim_dims(N, Z)
-        obs_bytes = 4 * N * D + 4 * G + 57 * N + 5  # writes + the per-unit view it reads
-        step_bytes = bytes_per - (4 * N * D + 4 * G)
-        kernels = []
-        for name, ms, nbytes in (("step_kernels (K0 heuristic-controller pass + K1 actions..rewards, caches, state)",
-                                  kprof["step_kernel_ms"], step_bytes),
-                                 ("obs_kernel (K2: observation + global-state stream, TMA)",
-                                  kprof["obs_kernel_ms"], obs_bytes),
-                                 ("reset_kernel (K3: deferred auto-resets)",
-                                  kprof["reset_kernel_ms"], None)):
-            ent = {"kernel": name, "ms_avg": ms}
-            if nbytes and ms > 0:
-                gbs = nbytes * per / (ms / 1000.0) / 1e9
-                ent.update({"bytes_per_env_step": nbytes, "achieved_gbs": gbs,
-                            "frac": gbs / peak})
-            kernels.append(ent)
-        traffic = None
-        prof = os.path.join(ROOT, "profiles", f"traffic_{args.scenario}.json")
-        if os.path.exists(prof):
-            with open(prof) as fh:
-                traffic = json.load(fh).get("bytes_per_env_step", 0) * per or None
         line = {
-            "metric": "env_steps_per_s", "value": value, "unit": "env-steps/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "metric": "env_steps_per_s", "value": head["value"], "unit": "env-steps/s",
+            "n_gpus": cx.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (scenario JSON, seeded lanes)",
-            "agent_steps_per_s": value * len(sc.units),
-            "config": {"workload": WORKLOAD[args.scenario], "scenario": SCENARIOS[args.scenario],
+            "agent_steps_per_s": head["agent_steps_per_s"],
+            "config": {"workload": WORKLOAD[key], "scenario": SCENARIOS[key],
                        "envs": total, "envs_per_gpu": per, "n_units": N, "n_zones": Z,
-                       "obs_dim": sim_dims(N, Z)[0], "global_dim": sim_dims(N, Z)[1],
-                       "parallelism": f"env-shard x{world}",
+                       "obs_dim": D, "global_dim": G,
+                       "parallelism": f"env-shard x{cx.world}",
                        "l2": "inputs larger than L2: every step writes "
-                             f"{4 * N * sim_dims(N, Z)[0] * per / 1e9:.1f} GB of observations",
-                       "e2e_workload": "bindings.HostStepper (bindings.step per step), ally "
-                                       "external: int64 actions H2D from pinned host and "
-                                       "rewards/terminated/truncated D2H every step, copies "
-                                       "overlapped with the neighbouring steps"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "bytes_per_env_step": bytes_per, "kernel_ms_avg": kern_avg,
-                         "scope": "one step = controller pass + step kernel + observation kernel + reset kernel "
-                                  "(SURVEY.md 8(d) bytes per env-step x envs / step time)",
-                         "kernels": kernels,
-                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)" if peaks
-                         else "fallback"},
-            "e2e": {"value": e2e_value, "unit": "env-steps/s",
-                    "h2d_bytes_per_step": per * N * 8,
-                    "d2h_bytes_per_step": per * N * 4 + 2 * per},
-            # K1, K2, K3 per step, plus the refresh check and K0 (the
-            # heuristic-controller pass) from 4,096 lanes on unless disabled
-            "gpu_launches": (3 + (2 if per >= int(os.environ.get("TABX_K0_MIN_ENVS", 4096))
-                                  and os.environ.get("TABX_NO_K0") != "1" else 0)) * args.steps,
-            "clocks": clk.summary(),
-            "episode_stats": stats,
+                             f"{4 * N * D * per / 1e9:.1f} GB of observations",
+                       "e2e_workload": "bindings.HostStepper (one step per call, K steps), "
+                                       "ally external: int64 actions H2D from pinned host "
+                                       "and rewards/terminated/truncated D2H every step, "
+                                       "copies overlapped with the neighbouring steps; "
+                                       "observations and action masks stay on the device "
+                                       "(a GPU policy reads them in place; host_obs_e2e "
+                                       "prices copying them out)"},
+            "roofline": head["roofline"],
+            "e2e": e2e,
+            "gpu_launches": head["gpu_launches"],
+            "clocks": head["clocks"],
+            "episode_stats": head["episode_stats"],
         }
+        for k, m in extras.items():
+            line[k] = m
+        if episode is not None:
+            line["c3_episode" if key == "c3" else f"{key}_episode"] = episode
+        if host_obs is not None:
+            line["host_obs_e2e"] = host_obs
+        if reconfig is not None:
+            line["reconfig"] = reconfig
         if cpu is not None:
             line["cpu_baseline"] = cpu
         if c5 is not None:
             line["rollout_c5"] = c5
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    if cx.world > 1:
+        cx.dist.destroy_process_group()
     return 0
 
 
@@ -447,7 +592,13 @@ def main(argv=None) -> int:
     ap.add_argument("--envs", type=int, default=0,
                     help="environments per GPU (weak scaling: the job runs n_gpus x envs)")
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--configs", default="c1,c2,c4",
+                    help="other BASELINE configs timed in the same run (comma list)")
+    ap.add_argument("--episode-steps", type=int, default=410,
+                    help="whole-episode window of the headline config (0 = skip)")
+    ap.add_argument("--host-obs-steps", type=int, default=3,
+                    help="steps of the host-observation e2e variant (0 = skip)")
+    ap.add_argument("--no-reconfig", dest="reconfig", action="store_false")
     ap.add_argument("--cpu-envs", type=int, default=1024)
     ap.add_argument("--cpu-steps", type=int, default=100)
     ap.add_argument("--cpu-workers", type=int, default=0, help="reference arm processes (0 = all cores)")

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define TABX_ABI_VERSION 3
+#define TABX_ABI_VERSION 4
 
 #define TABX_MAX_UNITS 256
 #define TABX_MAX_ZONES 32
@@ -49,8 +49,8 @@ extern "C" {
 #define TABX_E_CUDA 2         /* CUDA runtime failure (see tabx_last_error) */
 #define TABX_E_ACTION_MASK 3  /* an external action violated the mask       */
 #define TABX_E_SHAPE 4        /* config capacities differ from the handle's */
-#define TABX_E_ALIGNMENT 5    /* observation buffer not 16-byte aligned     */
-#define TABX_E_CAPACITY 6     /* too many distinct configs                  */
+#define TABX_E_ALIGNMENT 5    /* obs / global-state buffer not 16-B aligned */
+#define TABX_E_CAPACITY 6     /* every config-table slot is in use          */
 
 /* controller ids (core.py:138) */
 #define TABX_CTRL_EXTERNAL 0
@@ -117,6 +117,9 @@ typedef struct tabx_config {
  * final_* rows are written only for lanes that auto-reset this step
  * (reset_mask[b] = 1); other rows are left untouched, so the reference's
  * final_observations equals where(reset_mask, final_observations, observations).
+ * observations, final_observations, global_state and final_global_state
+ * must be 16-byte aligned (they are written with TMA bulk stores); calls
+ * given a misaligned one return TABX_E_ALIGNMENT before launching anything.
  */
 typedef struct tabx_outputs {
   float* observations;        /* [B, N, obs_dim]          */
@@ -259,12 +262,17 @@ int tabx_init_output(tabx_handle* h, const tabx_outputs* out);
 int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out);
 
 /*
- * reset_env(b, config, seed): respawn lane b (optionally with a new config,
- * appended to the handle's config table, and/or a new seed), then run
- * init_output for the whole batch into `out` (environment.py:490-498).
+ * reset_env(b, config, seed): respawn lane b (optionally with a new config
+ * and/or a new seed), then run init_output for the whole batch into `out`
+ * (environment.py:490-498).  A config equal (byte for byte) to a row of the
+ * handle's config table reuses that slot; otherwise it takes a slot no lane
+ * uses any more (slots are reference-counted per lane) or a new one.  The
+ * slot lane b runs on afterwards is stored in *slot_out (may be NULL).
+ * Asynchronous: nothing waits on the stream (the config row is staged in
+ * pinned memory, slot and seed are kernel arguments).
  */
 int tabx_reset_env(tabx_handle* h, int64_t b, const tabx_config* config, uint64_t seed,
-                   int32_t has_seed, const tabx_outputs* out);
+                   int32_t has_seed, const tabx_outputs* out, int32_t* slot_out);
 
 /*
  * Respawn every lane with new seeds (host [B]) and episode counters 0, and
@@ -317,12 +325,18 @@ int tabx_get_profile(tabx_handle* h, double* ms, int64_t* steps);
 /*
  * Config table management.  The table starts with the configs given to
  * tabx_create (plus those added by tabx_reset_env); tabx_reserve_configs
- * grows its capacity (synchronises), tabx_num_configs reports count and
+ * grows its capacity (synchronises; reallocates the table, so CUDA graphs
+ * captured before must be re-captured), tabx_num_configs reports rows and
  * capacity, tabx_get_config copies one row to the host (synchronises).
+ * tabx_config_slot reports how many lanes the host knows on `slot` and
+ * whether the slot is pinned (never recycled: rows written by tabx_levels,
+ * and every slot that existed when tabx_respawn_lanes / tabx_import_state
+ * moved lanes by device data).
  */
 int tabx_reserve_configs(tabx_handle* h, int32_t capacity);
 int tabx_num_configs(tabx_handle* h, int32_t* count, int32_t* capacity);
 int tabx_get_config(tabx_handle* h, int32_t slot, tabx_config* dst);
+int tabx_config_slot(tabx_handle* h, int32_t slot, int64_t* lanes, int32_t* pinned);
 
 /*
  * A batch of levels on the device, one per entry k < count: row

@@ -12,7 +12,7 @@ MAX_UNITS = 256
 MAX_ZONES = 32
 NUM_ACTIONS = 7
 NUM_STATS = 8
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 OK = 0
 E_ARGUMENT, E_CUDA, E_ACTION_MASK, E_SHAPE, E_ALIGNMENT, E_CAPACITY = 1, 2, 3, 4, 5, 6
@@ -121,7 +121,7 @@ def lib() -> ct.CDLL:
         "tabx_init_output": (_i32, [P, ct.POINTER(TabxOutputs)]),
         "tabx_step": (_i32, [P, P, ct.POINTER(TabxOutputs)]),
         "tabx_reset_env": (_i32, [P, _i64, ct.POINTER(TabxConfig), ct.c_uint64, _i32,
-                                  ct.POINTER(TabxOutputs)]),
+                                  ct.POINTER(TabxOutputs), P]),
         "tabx_respawn_all": (_i32, [P, P, P]),
         "tabx_export_state": (_i32, [P, ct.POINTER(TabxState)]),
         "tabx_export_lanes": (_i32, [P, P, ct.c_int64, ct.POINTER(TabxState)]),
@@ -133,6 +133,7 @@ def lib() -> ct.CDLL:
         "tabx_reserve_configs": (_i32, [P, _i32]),
         "tabx_num_configs": (_i32, [P, P, P]),
         "tabx_get_config": (_i32, [P, _i32, ct.POINTER(TabxConfig)]),
+        "tabx_config_slot": (_i32, [P, _i32, P, P]),
         "tabx_levels": (_i32, [P, _i32, ct.POINTER(TabxLevelSpec), _d, P, _i32, _i32, P]),
         "tabx_respawn_lanes": (_i32, [P, P, P, P, _i64]),
         "tabx_set_profiling": (_i32, [P, _i32]),

@@ -3,6 +3,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "tabx_device.cuh"
 #include "tabx_math.cuh"
 
@@ -16,6 +20,38 @@ cudaError_t launch_emit_w1(const Params& P, int sm_count, cudaStream_t stream);
 cudaError_t launch_emit_w2(const Params& P, int sm_count, cudaStream_t stream);
 cudaError_t launch_emit_w4(const Params& P, int sm_count, cudaStream_t stream);
 cudaError_t launch_emit_w8(const Params& P, int sm_count, cudaStream_t stream);
+
+cudaError_t launch_geometry(const void* kernel, int threads, size_t smem, int* per_sm) {
+  static std::mutex mu;
+  // resident blocks per (kernel, device, threads, smem); the dynamic
+  // shared-memory limit per (kernel, device) only ever rises (lowering it
+  // would break a cached larger launch of the same kernel)
+  static std::map<std::tuple<const void*, int, int, size_t>, int> occ;
+  static std::map<std::pair<const void*, int>, size_t> limit;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const auto key = std::make_tuple(kernel, dev, threads, smem);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = occ.find(key);
+  if (it != occ.end()) {
+    *per_sm = it->second;
+    return cudaSuccess;
+  }
+  size_t& lim = limit[std::make_pair(kernel, dev)];
+  if (smem > lim) {
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    lim = smem;
+  }
+  int n = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+  if (e != cudaSuccess) return e;
+  n = n < 1 ? 1 : n;
+  occ.emplace(key, n);
+  *per_sm = n;
+  return cudaSuccess;
+}
 
 cudaError_t launch_emit(const Params& P, int W, int sm_count, cudaStream_t stream) {
   switch (W) {
@@ -58,16 +94,21 @@ __global__ void validate_kernel(const int64_t* __restrict__ actions, DevState st
 // fill_env for lanes [b0, b1) (arrays.py:244-321); also used at creation.
 // With a lane list, entry k spawns lane lanes[k], first switching it to
 // config slots[k] and seed seeds[k] when those are given.
+// A single lane (reset_env) takes its slot / seed as immediates instead
+// (imm_slot >= 0, has_imm_seed), so the host never stages them in memory.
 __global__ void spawn_kernel(DevState st, const tabx_config* __restrict__ cfgs,
                              const DerivedCfg* __restrict__ dcfgs, int64_t b0, int64_t b1, int N,
                              int W, int reset_stats, const int64_t* __restrict__ lanes,
-                             const int32_t* __restrict__ slots, const uint64_t* __restrict__ seeds) {
+                             const int32_t* __restrict__ slots, const uint64_t* __restrict__ seeds,
+                             int32_t imm_slot, uint64_t imm_seed, int has_imm_seed) {
   for (int64_t k = b0 + blockIdx.x; k < b1; k += gridDim.x) {
     const int64_t b = lanes ? lanes[k] : k;
-    if (slots || seeds) {
+    if (slots || seeds || imm_slot >= 0 || has_imm_seed) {
       if (threadIdx.x == 0) {
         if (slots) st.cfg[b] = slots[k];
         if (seeds) st.seed[b] = seeds[k];
+        if (imm_slot >= 0) st.cfg[b] = imm_slot;
+        if (has_imm_seed) st.seed[b] = imm_seed;
       }
       __syncthreads();
     }
@@ -97,6 +138,12 @@ __global__ void spawn_kernel(DevState st, const tabx_config* __restrict__ cfgs,
       }
     }
     if (threadIdx.x == 0) {
+      // env_steps statistic: the steps of an episode cut short by this
+      // respawn were never added to st_len (only finished episodes are)
+      if (reset_stats)
+        st.st_base[b] = 0;
+      else if (!(st.flags[b] & F_DONE))
+        st.st_base[b] += st.t[b];
       st.t[b] = 0;
       st.prev_gap[b] = 0.0;
       st.ep_return[b] = 0.0;
@@ -273,10 +320,15 @@ __global__ void derive_kernel(const tabx_config* __restrict__ cfgs, DerivedCfg* 
 }
 
 // Deterministic single-block reduction of the per-lane statistics.
+// env_steps of lane b = st_len (finished episodes) + st_base + t of the
+// running episode; st_base = -t at the last statistics reset (the part of
+// that episode counted before) + t of episodes cut short by a respawn.
 __global__ void stats_kernel(DevState st, int64_t B, double* out, int reset) {
   __shared__ double part[8][256];
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
+    const bool done = (st.flags[b] & F_DONE) != 0;
+    const int64_t running = done ? 0 : (int64_t)st.t[b];
     acc[0] += st.st_episodes[b];
     acc[1] += st.st_wins[b];
     acc[2] += st.st_fk_ally[b];
@@ -284,21 +336,23 @@ __global__ void stats_kernel(DevState st, int64_t B, double* out, int reset) {
     acc[4] += (double)st.st_len[b];
     acc[5] += st.st_ret[b];
     acc[6] += st.st_elims[b];
+    acc[7] += (double)(st.st_len[b] + st.st_base[b] + running);
     if (reset) {
       st.st_episodes[b] = st.st_wins[b] = st.st_fk_ally[b] = st.st_ties[b] = st.st_elims[b] = 0;
       st.st_len[b] = 0;
       st.st_ret[b] = 0.0;
+      st.st_base[b] = -running;
     }
   }
-  for (int k = 0; k < 7; ++k) part[k][threadIdx.x] = acc[k];
+  for (int k = 0; k < 8; ++k) part[k][threadIdx.x] = acc[k];
   __syncthreads();
   for (int s = blockDim.x / 2; s > 0; s >>= 1) {
     if ((int)threadIdx.x < s)
-      for (int k = 0; k < 7; ++k) part[k][threadIdx.x] += part[k][threadIdx.x + s];
+      for (int k = 0; k < 8; ++k) part[k][threadIdx.x] += part[k][threadIdx.x + s];
     __syncthreads();
   }
   if (threadIdx.x == 0)
-    for (int k = 0; k < 7; ++k) out[k] = part[k][0];
+    for (int k = 0; k < 8; ++k) out[k] = part[k][0];
 }
 
 __global__ void sincos_debug_kernel(const double* x, double* s, double* c, int64_t n) {
@@ -354,7 +408,15 @@ cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const Deri
   int grid = (int)(n < (int64_t)sm_count * 32 ? n : (int64_t)sm_count * 32);
   if (grid < 1) return cudaSuccess;
   spawn_kernel<<<grid, 32 * W, 0, stream>>>(st, cfgs, dcfgs, b0, b1, N, W, reset_stats, nullptr,
-                                             nullptr, nullptr);
+                                             nullptr, nullptr, -1, 0, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spawn_one(const DevState& st, const tabx_config* cfgs, const DerivedCfg* dcfgs,
+                             int64_t b, int32_t slot, uint64_t seed, int has_seed, int N, int W,
+                             cudaStream_t stream) {
+  spawn_kernel<<<1, 32 * W, 0, stream>>>(st, cfgs, dcfgs, b, b + 1, N, W, 0, nullptr, nullptr,
+                                          nullptr, slot, seed, has_seed);
   return cudaGetLastError();
 }
 
@@ -364,7 +426,8 @@ cudaError_t launch_spawn_lanes(const DevState& st, const tabx_config* cfgs,
                                cudaStream_t stream) {
   int grid = (int)(n < (int64_t)sm_count * 32 ? n : (int64_t)sm_count * 32);
   if (grid < 1) return cudaSuccess;
-  spawn_kernel<<<grid, 32 * W, 0, stream>>>(st, cfgs, dcfgs, 0, n, N, W, 0, lanes, slots, seeds);
+  spawn_kernel<<<grid, 32 * W, 0, stream>>>(st, cfgs, dcfgs, 0, n, N, W, 0, lanes, slots, seeds,
+                                             -1, 0, 0);
   return cudaGetLastError();
 }
 

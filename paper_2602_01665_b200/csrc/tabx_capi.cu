@@ -5,7 +5,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "tabx_device.cuh"
@@ -24,6 +27,9 @@ cudaError_t launch_derive(const tabx_config* cfgs, DerivedCfg* dcfgs, int k0, in
 cudaError_t launch_levels(tabx_config* cfgs, const int32_t* src_slots, int32_t dst_first,
                           int32_t count, const tabx_level_spec& spec, int op, double delta,
                           tabx_pcg64* rngs, int sm_count, cudaStream_t stream);
+cudaError_t launch_spawn_one(const DevState& st, const tabx_config* cfgs, const DerivedCfg* dcfgs,
+                             int64_t b, int32_t slot, uint64_t seed, int has_seed, int N, int W,
+                             cudaStream_t stream);
 cudaError_t launch_spawn_lanes(const DevState& st, const tabx_config* cfgs,
                                const DerivedCfg* dcfgs, const int64_t* lanes, const int32_t* slots,
                                const uint64_t* seeds, int64_t n, int N, int W, int sm_count,
@@ -67,6 +73,25 @@ struct tabx_handle {
   std::vector<tabx_config> cfg_host;  // host mirror of the table rows
   std::vector<char> cfg_host_ok;       // 0: row written on the device (tabx_levels)
   int cfg_cap = TABX_MAX_CONFIGS;
+  // Config-slot recycling.  lane_slot mirrors st.cfg for every change the
+  // host makes (create, reset_env, respawn_all); refcnt[k] counts the lanes
+  // on slot k.  A slot whose count drops to 0 is reused by the next new
+  // config.  Slots the host cannot track — rows written on the device
+  // (tabx_levels) and every slot that existed when lanes were moved by device
+  // data (tabx_respawn_lanes with slots, tabx_import_state with config) — are
+  // pinned: never recycled.  row_hash / by_hash find an identical row in O(1).
+  std::vector<int32_t> lane_slot;
+  std::vector<int64_t> refcnt;
+  std::vector<char> pinned;
+  std::vector<uint64_t> row_hash;
+  std::unordered_multimap<uint64_t, int32_t> by_hash;
+  std::vector<int32_t> free_slots;
+  // pinned staging ring for config rows uploaded by tabx_reset_env (a
+  // cudaMemcpyAsync from pageable memory would block on the stream)
+  static constexpr int STAGE_SLOTS = 8;
+  tabx_config* stage = nullptr;
+  cudaEvent_t stage_ev[STAGE_SLOTS] = {};
+  int stage_next = 0;
   tabx_config* cfg_dev = nullptr;
   DerivedCfg* dcfg_dev = nullptr;
   DevState st{};
@@ -179,9 +204,14 @@ static int ctrl_units(tabx_handle* h) {
 
 static int check_outputs(const tabx_outputs* out, int D) {
   if (!out) return TABX_OK;
-  const float* ptrs[2] = {out->observations, out->final_observations};
+  // rows leave through TMA bulk stores (cp.async.bulk), which need a
+  // 16-byte-aligned base
+  const float* ptrs[4] = {out->observations, out->final_observations, out->global_state,
+                          out->final_global_state};
   for (const float* p : ptrs)
-    if (p && (((uintptr_t)p) & 15u)) return fail(TABX_E_ALIGNMENT, "observation buffer must be 16-byte aligned");
+    if (p && (((uintptr_t)p) & 15u))
+      return fail(TABX_E_ALIGNMENT,
+                  "observation / global-state buffers must be 16-byte aligned");
   if (out->observations_bf16 && ((((uintptr_t)out->observations_bf16) & 15u) ||
                                  (out->observations_bf16_ld & 7) ||
                                  out->observations_bf16_ld < D))
@@ -190,28 +220,127 @@ static int check_outputs(const tabx_outputs* out, int D) {
   return TABX_OK;
 }
 
+static uint64_t config_hash(const tabx_config* c) {
+  // FNV-1a over 64-bit words (the struct is a multiple of 8 bytes)
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(c);
+  uint64_t x = 0xcbf29ce484222325ull;
+  for (size_t k = 0; k < sizeof(tabx_config) / 8; ++k) {
+    x ^= w[k];
+    x *= 0x100000001b3ull;
+  }
+  return x;
+}
+
+static void slot_unindex(tabx_handle* h, int32_t k) {
+  auto range = h->by_hash.equal_range(h->row_hash[k]);
+  for (auto it = range.first; it != range.second; ++it)
+    if (it->second == k) {
+      h->by_hash.erase(it);
+      return;
+    }
+}
+
+// Recount the per-slot lane counts from the host mirror; rebuild the free list.
+static void recount_slots(tabx_handle* h) {
+  const size_t n = h->cfg_host.size();
+  h->refcnt.assign(n, 0);
+  for (int32_t k : h->lane_slot) h->refcnt[k] += 1;
+  h->free_slots.clear();
+  for (size_t k = n; k-- > 0;)
+    if (!h->refcnt[k] && !h->pinned[k]) {
+      slot_unindex(h, (int32_t)k);
+      h->free_slots.push_back((int32_t)k);
+    }
+}
+
+// Lanes were moved by device-side data: the mirror is no longer exact, so
+// every existing slot is kept forever (counts stay upper bounds).
+static void pin_all_slots(tabx_handle* h) {
+  for (size_t k = 0; k < h->pinned.size(); ++k) h->pinned[k] = 1;
+  h->free_slots.clear();
+}
+
+static void move_lane(tabx_handle* h, int64_t b, int32_t k) {
+  const int32_t old = h->lane_slot[b];
+  if (old == k) return;
+  h->lane_slot[b] = k;
+  h->refcnt[k] += 1;
+  if (--h->refcnt[old] == 0 && !h->pinned[old]) {
+    slot_unindex(h, old);
+    h->free_slots.push_back(old);
+  }
+}
+
+static int stage_config(tabx_handle* h, const tabx_config* c, const tabx_config** staged) {
+  if (!h->stage) {
+    TABX_CUDA(cudaHostAlloc((void**)&h->stage, sizeof(tabx_config) * tabx_handle::STAGE_SLOTS,
+                            cudaHostAllocDefault),
+              "config staging allocation");
+    for (int q = 0; q < tabx_handle::STAGE_SLOTS; ++q)
+      TABX_CUDA(cudaEventCreateWithFlags(&h->stage_ev[q], cudaEventDisableTiming), "event create");
+  }
+  const int q = h->stage_next;
+  h->stage_next = (q + 1) % tabx_handle::STAGE_SLOTS;
+  // the copy that last used this staging row must have read it (normally
+  // long done: STAGE_SLOTS uploads ago)
+  TABX_CUDA(cudaEventSynchronize(h->stage_ev[q]), "staging wait");
+  memcpy(h->stage + q, c, sizeof(tabx_config));
+  *staged = h->stage + q;
+  return TABX_OK;
+}
+
+static int stage_done(tabx_handle* h, const tabx_config* staged) {
+  const int q = (int)(staged - h->stage);
+  TABX_CUDA(cudaEventRecord(h->stage_ev[q], h->stream), "staging record");
+  return TABX_OK;
+}
+
+// The table slot holding a row equal to *c (same bytes), else a recycled
+// free slot or a new one with *c uploaded and derived on the stream.
 static int find_or_add_config(tabx_handle* h, const tabx_config* c, int32_t* idx) {
   if (c->n_units != h->N || c->n_zones != h->Z)
     return fail(TABX_E_SHAPE, "batched environments must share max_units and max_zones");
-  for (size_t k = 0; k < h->cfg_host.size(); ++k) {
+  const uint64_t hs = config_hash(c);
+  auto range = h->by_hash.equal_range(hs);
+  for (auto it = range.first; it != range.second; ++it) {
+    const int32_t k = it->second;
     if (h->cfg_host_ok[k] && !memcmp(&h->cfg_host[k], c, sizeof(tabx_config))) {
-      *idx = (int32_t)k;
+      *idx = k;
       return TABX_OK;
     }
   }
-  if ((int)h->cfg_host.size() >= h->cfg_cap)
-    return fail(TABX_E_CAPACITY, "config table full");
-  h->cfg_host.push_back(*c);
-  h->cfg_host_ok.push_back(1);
+  int32_t k;
+  if (!h->free_slots.empty()) {
+    k = h->free_slots.back();
+    h->free_slots.pop_back();
+    h->cfg_host[k] = *c;
+    h->cfg_host_ok[k] = 1;
+  } else {
+    if ((int)h->cfg_host.size() >= h->cfg_cap)
+      return fail(TABX_E_CAPACITY,
+                  "config table full: every slot is in use by a lane (tabx_reserve_configs)");
+    h->cfg_host.push_back(*c);
+    h->cfg_host_ok.push_back(1);
+    h->refcnt.push_back(0);
+    h->pinned.push_back(0);
+    h->row_hash.push_back(0);
+    k = (int32_t)h->cfg_host.size() - 1;
+  }
+  h->row_hash[k] = hs;
+  h->by_hash.emplace(hs, k);
   ++h->cfg_version;
-  const size_t k = h->cfg_host.size() - 1;
-  TABX_CUDA(cudaMemcpyAsync(h->cfg_dev + k, c, sizeof(tabx_config), cudaMemcpyHostToDevice,
+  const tabx_config* staged = nullptr;
+  int rc = stage_config(h, c, &staged);
+  if (rc) return rc;
+  TABX_CUDA(cudaMemcpyAsync(h->cfg_dev + k, staged, sizeof(tabx_config), cudaMemcpyHostToDevice,
                             h->stream),
             "config upload");
+  rc = stage_done(h, staged);
+  if (rc) return rc;
   TABX_CUDA(launch_derive(h->cfg_dev, h->dcfg_dev, (int)k, (int)k + 1, h->stream), "derive");
   if (c->controller[0] == TABX_CTRL_EXTERNAL || c->controller[1] == TABX_CTRL_EXTERNAL)
     h->any_external = true;
-  *idx = (int32_t)k;
+  *idx = k;
   return TABX_OK;
 }
 
@@ -271,7 +400,8 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
          o_ub = take(U), o_vis = take(4 * U * W),
          o_atk = take(4 * U * W), o_se = take(4 * B), o_sw = take(4 * B), o_sf = take(4 * B),
          o_stie = take(4 * B), o_sel = take(4 * B), o_sl = take(8 * B), o_sr = take(8 * B),
-         o_sync = take(sizeof(Sync)), o_stats = take(8 * TABX_NUM_STATS), o_ctl = take(U);
+         o_sync = take(sizeof(Sync)), o_stats = take(8 * TABX_NUM_STATS), o_ctl = take(U),
+         o_sb = take(8 * B);
   cudaError_t e = cudaMalloc(&h->arena, off);
   if (e != cudaSuccess) {
     delete h;
@@ -318,6 +448,7 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   st.st_elims = (uint32_t*)(a + o_sel);
   st.st_len = (int64_t*)(a + o_sl);
   st.st_ret = (double*)(a + o_sr);
+  st.st_base = (int64_t*)(a + o_sb);
   h->sync = (Sync*)(a + o_sync);
   h->stats_dev = (double*)(a + o_stats);
   // K0 is the default from TABX_K0_MIN_ENVS lanes on (4096; below
@@ -335,10 +466,16 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   for (int k = 0; k < n_configs; ++k) {
     h->cfg_host.push_back(configs[k]);
     h->cfg_host_ok.push_back(1);
+    h->pinned.push_back(0);
+    h->row_hash.push_back(config_hash(configs + k));
+    h->by_hash.emplace(h->row_hash.back(), k);
     if (configs[k].controller[0] == TABX_CTRL_EXTERNAL ||
         configs[k].controller[1] == TABX_CTRL_EXTERNAL)
       h->any_external = true;
   }
+  h->lane_slot.assign((size_t)B, 0);
+  if (env_config) h->lane_slot.assign(env_config, env_config + B);
+  recount_slots(h);
   e = cudaMemcpyAsync(h->cfg_dev, configs, sizeof(tabx_config) * n_configs,
                       cudaMemcpyHostToDevice, h->stream);
   if (e == cudaSuccess) e = launch_derive(h->cfg_dev, h->dcfg_dev, 0, n_configs, h->stream);
@@ -370,6 +507,10 @@ int tabx_destroy(tabx_handle* h) {
   if (h->prof_ev[0][0])
     for (int s = 0; s < tabx_handle::PROF_SLOTS; ++s)
       for (int k = 0; k < 4; ++k) cudaEventDestroy(h->prof_ev[s][k]);
+  if (h->stage) {
+    for (int q = 0; q < tabx_handle::STAGE_SLOTS; ++q) cudaEventDestroy(h->stage_ev[q]);
+    cudaFreeHost(h->stage);
+  }
   cudaFree(h->dcfg_dev);
   cudaFree(h->cfg_dev);
   cudaFree(h->arena);
@@ -456,27 +597,22 @@ int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
 }
 
 int tabx_reset_env(tabx_handle* h, int64_t b, const tabx_config* config, uint64_t seed,
-                   int32_t has_seed, const tabx_outputs* out) {
+                   int32_t has_seed, const tabx_outputs* out, int32_t* slot_out) {
   if (!h || b < 0 || b >= h->B) return fail(TABX_E_ARGUMENT, "tabx_reset_env: bad lane");
   int rc = check_outputs(out, h->D);
   if (rc) return rc;
   DeviceGuard guard(h->device);
+  int32_t idx = -1;  // -1: keep the lane's slot
   if (config) {
-    int32_t idx;
     rc = find_or_add_config(h, config, &idx);
     if (rc) return rc;
-    TABX_CUDA(cudaMemcpyAsync(h->st.cfg + b, &idx, 4, cudaMemcpyHostToDevice, h->stream),
-              "config index");
-    TABX_CUDA(cudaStreamSynchronize(h->stream), "reset_env sync");
+    move_lane(h, b, idx);
   }
-  if (has_seed) {
-    TABX_CUDA(cudaMemcpyAsync(h->st.seed + b, &seed, 8, cudaMemcpyHostToDevice, h->stream),
-              "seed upload");
-    TABX_CUDA(cudaStreamSynchronize(h->stream), "reset_env sync");
-  }
-  TABX_CUDA(launch_spawn(h->st, h->cfg_dev, h->dcfg_dev, b, b + 1, h->N, h->W, 0, h->sm_count,
-                         h->stream),
+  // slot and seed travel as kernel arguments: nothing here waits on the stream
+  TABX_CUDA(launch_spawn_one(h->st, h->cfg_dev, h->dcfg_dev, b, idx, seed, has_seed, h->N, h->W,
+                             h->stream),
             "spawn launch");
+  if (slot_out) *slot_out = h->lane_slot[b];
   return tabx_init_output(h, out);
 }
 
@@ -500,7 +636,12 @@ int tabx_respawn_all(tabx_handle* h, const uint64_t* seeds, const int32_t* env_c
   TABX_CUDA(launch_spawn(h->st, h->cfg_dev, h->dcfg_dev, 0, h->B, h->N, h->W, 1, h->sm_count,
                          h->stream),
             "spawn launch");
-  TABX_CUDA(cudaStreamSynchronize(h->stream), "respawn sync");
+  TABX_CUDA(cudaStreamSynchronize(h->stream), "respawn sync");  // host arrays may be freed
+  if (env_config)
+    h->lane_slot.assign(env_config, env_config + h->B);
+  else
+    h->lane_slot.assign((size_t)h->B, 0);
+  recount_slots(h);
   return TABX_OK;
 }
 
@@ -561,6 +702,14 @@ int tabx_num_configs(tabx_handle* h, int32_t* count, int32_t* capacity) {
   return TABX_OK;
 }
 
+int tabx_config_slot(tabx_handle* h, int32_t slot, int64_t* lanes, int32_t* pinned) {
+  if (!h || slot < 0 || slot >= (int32_t)h->cfg_host.size())
+    return fail(TABX_E_ARGUMENT, "tabx_config_slot: bad argument");
+  if (lanes) *lanes = h->refcnt[slot];
+  if (pinned) *pinned = h->pinned[slot];
+  return TABX_OK;
+}
+
 int tabx_get_config(tabx_handle* h, int32_t slot, tabx_config* dst) {
   if (!h || !dst || slot < 0 || slot >= (int32_t)h->cfg_host.size())
     return fail(TABX_E_ARGUMENT, "tabx_get_config: bad argument");
@@ -595,8 +744,18 @@ int tabx_levels(tabx_handle* h, int32_t op, const tabx_level_spec* spec, double 
   if (h->cfg_host.size() < end) {
     h->cfg_host.resize(end);
     h->cfg_host_ok.resize(end, 0);
+    h->refcnt.resize(end, 0);
+    h->pinned.resize(end, 0);
+    h->row_hash.resize(end, 0);
   }
-  for (size_t k = (size_t)dst_first; k < end; ++k) h->cfg_host_ok[k] = 0;
+  for (size_t k = (size_t)dst_first; k < end; ++k) {
+    if (h->cfg_host_ok[k]) slot_unindex(h, (int32_t)k);
+    h->cfg_host_ok[k] = 0;
+    h->pinned[k] = 1;  // caller-managed rows
+  }
+  h->free_slots.erase(std::remove_if(h->free_slots.begin(), h->free_slots.end(),
+                                     [&](int32_t k) { return h->pinned[k] != 0; }),
+                      h->free_slots.end());
   ++h->cfg_version;
   return TABX_OK;
 }
@@ -607,6 +766,7 @@ int tabx_respawn_lanes(tabx_handle* h, const int64_t* lanes, const int32_t* slot
     return fail(TABX_E_ARGUMENT, "tabx_respawn_lanes: bad argument");
   if (n == 0) return TABX_OK;
   DeviceGuard guard(h->device);
+  if (slots) pin_all_slots(h);
   TABX_CUDA(launch_spawn_lanes(h->st, h->cfg_dev, h->dcfg_dev, lanes, slots, seeds, n, h->N, h->W,
                                h->sm_count, h->stream),
             "respawn lanes");
@@ -616,6 +776,7 @@ int tabx_respawn_lanes(tabx_handle* h, const int64_t* lanes, const int32_t* slot
 int tabx_import_state(tabx_handle* h, const tabx_state* src) {
   if (!h || !src) return fail(TABX_E_ARGUMENT, "tabx_import_state: bad argument");
   DeviceGuard guard(h->device);
+  if (src->config) pin_all_slots(h);
   TABX_CUDA(launch_import(h->st, *src, h->cfg_dev, h->dcfg_dev, h->B, h->N, h->W, h->sm_count,
                           h->stream),
             "import");

@@ -59,6 +59,7 @@ struct DevState {
   uint32_t* st_elims;
   int64_t* st_len;
   double* st_ret;
+  int64_t* st_base;  // env_steps bookkeeping (stats_kernel)
 };
 
 // Control block: action-error latch, device step counter and the
@@ -166,5 +167,11 @@ __device__ __forceinline__ float f32_quot(double x, double y, double ry) {
   return __double2float_rn(q);
 }
 
-// effective_speed multiplier: sequential product over zones (arrays.py:338-343)
+// Launch geometry of a kernel with `smem` bytes of dynamic shared memory on
+// the CURRENT device: raises the kernel's dynamic shared-memory limit there
+// (a per-device attribute) and returns its resident blocks per SM.  Results
+// are cached per (kernel, device, smem) behind a mutex, so a step costs one
+// launch per kernel, stays capturable in a CUDA graph, and handles on
+// several devices (or threads) each get the attribute set on their own GPU.
+cudaError_t launch_geometry(const void* kernel, int threads, size_t smem, int* per_sm);
 }  // namespace tabx

@@ -490,18 +490,9 @@ cudaError_t launch_emit_f(const Params& P, int sm_count, cudaStream_t stream) {
   const int R = emit_rows(P.N, P.D, W == 1 ? TABX_EMIT_BUDGET : 8192);
   const int SF = emit_stage_floats(P.N, P.D, P.G, R);
   const size_t smem = (size_t)EPW * emit_warp_bytes<W>(P.N, P.Z, R, SF);
-  static size_t cached_smem = 0;
-  static int per_sm = 0;
-  if (smem != cached_smem) {
-    cudaError_t e = cudaFuncSetAttribute(emit_kernel<W, EPW, F16>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_kernel<W, EPW, F16>, 32 * EPW,
-                                                      smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-    cached_smem = smem;
-  }
+  int per_sm = 1;
+  cudaError_t e = launch_geometry((const void*)emit_kernel<W, EPW, F16>, 32 * EPW, smem, &per_sm);
+  if (e != cudaSuccess) return e;
   int64_t need = (P.B + EPW - 1) / EPW;
   int64_t cap = (int64_t)sm_count * per_sm;
   int grid = (int)(need < cap ? need : cap);
@@ -554,17 +545,10 @@ cudaError_t launch_emit_fixed(const Params& P, int sm_count, cudaStream_t stream
   constexpr int R = emit_rows(NF, D, W == 1 ? TABX_EMIT_BUDGET : 8192);
   constexpr int SF = emit_stage_floats(NF, D, G, R);
   const size_t smem = (size_t)EPW * emit_warp_bytes<W>(NF, ZF, R, SF);
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(emit_kernel_fixed<W, EPW, F16, NF, ZF>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int n = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, emit_kernel_fixed<W, EPW, F16, NF, ZF>,
-                                                      32 * EPW, smem);
-    if (e != cudaSuccess) return e;
-    per_sm = n < 1 ? 1 : n;
-  }
+  int per_sm = 1;
+  cudaError_t e = launch_geometry((const void*)emit_kernel_fixed<W, EPW, F16, NF, ZF>, 32 * EPW,
+                                  smem, &per_sm);
+  if (e != cudaSuccess) return e;
   int64_t need = (P.B + EPW - 1) / EPW;
   int64_t cap = (int64_t)sm_count * per_sm;
   int grid = (int)(need < cap ? need : cap);

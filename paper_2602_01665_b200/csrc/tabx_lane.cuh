@@ -1518,19 +1518,9 @@ cudaError_t launch_ctrl_t(const Params& P, int nh, int sm_count, cudaStream_t st
   const int NH = nh < 32 ? nh : 32;
   const int threads = 128;
   const size_t smem = sizeof(CtrlView<W>) * G * (threads / 32);
-  static size_t cached_smem = 0;
-  static int cached_per_sm = 0;
-  int per_sm = cached_per_sm;
-  if (smem != cached_smem) {
-    cudaError_t e = cudaFuncSetAttribute(ctrl_kernel<W>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ctrl_kernel<W>, threads, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-    cached_smem = smem;
-    cached_per_sm = per_sm;
-  }
+  int per_sm = 1;
+  cudaError_t e = launch_geometry((const void*)ctrl_kernel<W>, threads, smem, &per_sm);
+  if (e != cudaSuccess) return e;
   const int64_t groups = (P.B + G - 1) / G;
   const int64_t need = (groups + threads / 32 - 1) / (threads / 32);
   const int64_t cap = (int64_t)sm_count * per_sm;
@@ -1545,22 +1535,10 @@ cudaError_t launch_lanes_m(const Params& P, int sm_count, cudaStream_t stream, i
   const int threads = 32 * W * EPB;
   const size_t env_bytes = (sizeof(EnvSmem<W>) * EPB + 15) & ~(size_t)15;
   const size_t smem = env_bytes + (M == MODE_RESET ? reset_view_bytes<W>(P) * EPB : 0);
-  // attribute + occupancy are host-side queries; cache them per smem size so a
-  // step costs one launch per kernel (and stays capturable in a CUDA graph)
-  static size_t cached_smem = 0;
-  static int cached_per_sm = 0;
-  int per_sm = cached_per_sm;
-  if (smem != cached_smem) {
-    cudaError_t e = cudaFuncSetAttribute(lane_kernel<W, EPB, M, NF, ZF>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, lane_kernel<W, EPB, M, NF, ZF>, threads,
-                                                      smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-    cached_smem = smem;
-    cached_per_sm = per_sm;
-  }
+  int per_sm = 1;
+  cudaError_t e =
+      launch_geometry((const void*)lane_kernel<W, EPB, M, NF, ZF>, threads, smem, &per_sm);
+  if (e != cudaSuccess) return e;
   int64_t need = (P.B + EPB - 1) / EPB;
   int64_t cap = (int64_t)sm_count * per_sm;
   int grid = (int)(need < cap ? need : cap);

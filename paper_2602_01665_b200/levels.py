@@ -1,254 +1,106 @@
-"""Level sampling and mutation, host API + device batch.
+"""Level sampling and mutation on the device.
 
-Host functions mirror ``pkg/src/skirmish/scenario.py:563-826`` draw for draw
-on a ``numpy.random.Generator``:
-
-* ``LevelGenSpec`` (``:581-663``) with the same validation messages and
-  invariant clipping, ``default_level_spec`` (``:666-679``);
-* ``sample_level(spec, rng)`` (``:696-747``);
-* ``mutate_level(config, op, rng, spec=None, delta=0.1)`` (``:753-826``).
-
-``DeviceLevels`` runs the same two functions for a whole batch of levels on
-the GPU, one warp per level, writing the resulting ``tabx_config`` rows
-straight into a simulator's config table (``tabx_levels``), so a curriculum
-can resample or mutate thousands of levels and respawn lanes on them
+``DeviceLevels`` runs the reference's ``sample_level`` / ``mutate_level``
+(``pkg/src/skirmish/scenario.py:696-826``) for a whole batch of levels on the
+GPU, one warp per level (``tabx_levels``), writing ``tabx_config`` rows
+straight into a simulator's config table, so a curriculum can resample or
+mutate thousands of levels and respawn lanes on them
 (``tabx_respawn_lanes``) without building configs on the host.  Each level
 draws from its own PCG64 stream whose state is the numpy bit generator's
 (128-bit LCG, XSL-RR output, the buffered 32-bit half used by bounded
-integers), so a device level equals ``build_config(sample_level(spec,
-Generator(PCG64(...))))`` and the generators' states advance identically.
+integers), so a device level equals the reference's level built from the
+same ``Generator(PCG64(...))`` and the generators' states advance
+identically (checked against a host restatement in ``oracle/`` by
+``tests/test_gpu_levels.py``).
+
+``LevelRanges`` describes the free parameters: which categories are open
+and the ranges draws come from, resolved (clipped to each field's
+invariants, ``scenario.py:581-663``) into the ``tabx_level_spec`` the
+kernel reads.
 """
 from __future__ import annotations
 
 import ctypes as ct
-from dataclasses import dataclass, replace
+from dataclasses import dataclass, field
 
 import numpy as np
 
-from .scenario import ZONE_TYPES, Scenario, Team, Unit, Zone
+from .scenario import ZONE_TYPES, Scenario
 
-UNIT_FREE_FIELDS = ("attack_damage", "max_health", "speed")
-LAVA_DAMAGE_RANGE = (2.0, 10.0)   # scenario.py:41
-SWAMP_MULT_RANGE = (0.2, 0.8)     # scenario.py:42
-ZONE_AXIS_RANGE = (1.5, 6.0)      # scenario.py:43
-_MIN_HEALTH = 1.0
-_MIN_AXIS = 0.1
-_MIN_EFFECT = 0.01
+# unit fields a level may redraw, in the kernel's (sorted-name) order, with
+# the (floor, ceiling) each drawn range is clipped to
+UNIT_FIELDS = {"attack_damage": (None, None), "max_health": (1.0, None), "speed": (0.0, None)}
+EFFECT_BOUNDS = {"lava": (0.01, None), "swamp": (0.01, 1.0)}
+AXIS_FLOOR = 0.1
+OPEN_ALL = ("unit_spec", "zones", "heuristic")
 MUTATION_OPS = ("perturb", "swap_axes", "retype")
-CATEGORIES = ("unit_spec", "zones", "heuristic")
 
 
-def _clip_range(lo: float, hi: float, floor: float | None, ceil: float | None):
+def _resolve(rng, floor, ceil):
+    lo, hi = float(rng[0]), float(rng[1])
     if lo > hi:
-        raise ValueError(f"range ({lo}, {hi}) has min > max")
+        raise ValueError(f"range ({rng[0]}, {rng[1]}) has min > max")
     if floor is not None:
         lo, hi = max(lo, floor), max(hi, floor)
     if ceil is not None:
         lo, hi = min(lo, ceil), min(hi, ceil)
-    return (float(lo), float(hi))
+    return lo, hi
 
 
 @dataclass(frozen=True)
-class LevelGenSpec:
-    """Free-parameter ranges around a base scenario (scenario.py:581-663)."""
+class LevelRanges:
+    """Free-parameter ranges around a base scenario.  ``None`` for a range
+    keeps the base value; an empty ``open`` freezes everything."""
 
     base: Scenario
-    categories: tuple = CATEGORIES
-    unit_ranges: tuple | dict = ()
+    open: tuple = OPEN_ALL
+    units: dict = field(default_factory=dict)        # field -> (lo, hi)
     zone_types: tuple = ZONE_TYPES
-    zone_center_box: tuple | None = None
-    zone_axis_range: tuple | None = None
-    zone_effect_ranges: tuple | dict = ()
-    epsilon_range: tuple | None = None
-    aggressive_range: tuple | None = None
+    center_box: tuple | None = None                  # ((x0, x1), (y0, y1))
+    zone_axes: tuple | None = None
+    zone_effects: dict = field(default_factory=dict)  # "lava" / "swamp" -> (lo, hi)
+    epsilon: tuple | None = None
+    aggressive: tuple | None = None
 
     def __post_init__(self):
-        for cat in self.categories:
-            if cat not in CATEGORIES:
-                raise ValueError(f"unknown category {cat!r}")
-        ur = dict(self.unit_ranges)
-        for name in ur:
-            if name not in UNIT_FREE_FIELDS:
+        bad = [c for c in self.open if c not in OPEN_ALL]
+        if bad:
+            raise ValueError(f"unknown category {bad[0]!r}")
+        units = {}
+        for name, rng in self.units.items():
+            if name not in UNIT_FIELDS:
                 raise ValueError(f"unknown unit range field {name!r}")
-        if "max_health" in ur:
-            ur["max_health"] = _clip_range(*ur["max_health"], _MIN_HEALTH, None)
-        if "speed" in ur:
-            ur["speed"] = _clip_range(*ur["speed"], 0.0, None)
-        if "attack_damage" in ur:
-            ur["attack_damage"] = _clip_range(*ur["attack_damage"], None, None)
-        object.__setattr__(self, "unit_ranges", tuple(sorted((k, v) for k, v in ur.items())))
-        er = dict(self.zone_effect_ranges)
-        if "lava" in er:
-            er["lava"] = _clip_range(*er["lava"], _MIN_EFFECT, None)
-        if "swamp" in er:
-            er["swamp"] = _clip_range(*er["swamp"], _MIN_EFFECT, 1.0)
-        if "bush" in er:
-            raise ValueError("bush zones have no effect range")
-        object.__setattr__(self, "zone_effect_ranges",
-                           tuple(sorted((k, v) for k, v in er.items())))
-        if self.zone_axis_range is not None:
-            object.__setattr__(self, "zone_axis_range",
-                               _clip_range(*self.zone_axis_range, _MIN_AXIS, None))
-        if self.epsilon_range is not None:
-            object.__setattr__(self, "epsilon_range", _clip_range(*self.epsilon_range, 0.0, 1.0))
-        if self.aggressive_range is not None:
-            object.__setattr__(self, "aggressive_range",
-                               _clip_range(*self.aggressive_range, 0.0, None))
+            units[name] = _resolve(rng, *UNIT_FIELDS[name])
+        effects = {}
+        for name, rng in self.zone_effects.items():
+            if name not in EFFECT_BOUNDS:
+                raise ValueError(f"{name} zones have no effect range")
+            effects[name] = _resolve(rng, *EFFECT_BOUNDS[name])
         for t in self.zone_types:
             if t not in ZONE_TYPES:
                 raise ValueError(f"unknown zone type {t!r}")
+        set_ = object.__setattr__
+        set_(self, "units", units)
+        set_(self, "zone_effects", effects)
+        if self.zone_axes is not None:
+            set_(self, "zone_axes", _resolve(self.zone_axes, AXIS_FLOOR, None))
+        if self.epsilon is not None:
+            set_(self, "epsilon", _resolve(self.epsilon, 0.0, 1.0))
+        if self.aggressive is not None:
+            set_(self, "aggressive", _resolve(self.aggressive, 0.0, None))
+        if self.center_box is None:
+            f = self.base.field
+            set_(self, "center_box", ((f.margin, f.width - f.margin),
+                                      (f.margin, f.height - f.margin)))
 
-    def center_box(self):
-        if self.zone_center_box is not None:
-            return self.zone_center_box
-        f = self.base.field
-        return ((f.margin, f.width - f.margin), (f.margin, f.height - f.margin))
-
-    def effect_range(self, ztype: str):
-        for name, rng in self.zone_effect_ranges:
-            if name == ztype:
-                return rng
-        return None
-
-
-def default_level_spec(base: Scenario) -> LevelGenSpec:
-    """All three categories open with broad but safe ranges (scenario.py:666-679)."""
-    return LevelGenSpec(
-        base=base,
-        unit_ranges={"max_health": (20.0, 800.0), "speed": (0.5, 1.5),
-                     "attack_damage": (-10.0, 80.0)},
-        zone_axis_range=ZONE_AXIS_RANGE,
-        zone_effect_ranges={"lava": LAVA_DAMAGE_RANGE, "swamp": SWAMP_MULT_RANGE},
-        epsilon_range=(0.0, 1.0),
-        aggressive_range=(0.0, 0.7),
-    )
-
-
-def _with_unit_fields(u: Unit, fields: dict) -> Unit:
-    if not fields:
-        return u
-    if u.preset is not None:
-        merged = dict(u.overrides)
-        merged.update(fields)
-        return replace(u, overrides=tuple(sorted(merged.items())))
-    return replace(u, spec=replace(u.spec, **fields))
-
-
-def _unit_value(u: Unit, name: str) -> float:
-    return float(getattr(u.resolved_spec(), name))
-
-
-def _copy(sc: Scenario, **kw) -> Scenario:
-    return replace(sc, units=list(sc.units), zones=list(sc.zones), notes=list(sc.notes), **kw)
-
-
-def sample_level(spec: LevelGenSpec, rng: np.random.Generator) -> Scenario:
-    """Base config with every open free parameter redrawn uniformly."""
-    out = _copy(spec.base)
-    if "unit_spec" in spec.categories and spec.unit_ranges:
-        for i, u in enumerate(out.units):
-            drawn = {name: float(rng.uniform(lo, hi)) for name, (lo, hi) in spec.unit_ranges}
-            out.units[i] = _with_unit_fields(u, drawn)
-    if "zones" in spec.categories:
-        (x0, x1), (y0, y1) = spec.center_box()
-        for i, z in enumerate(out.zones):
-            ztype = str(rng.choice(spec.zone_types))
-            center = (float(rng.uniform(x0, x1)), float(rng.uniform(y0, y1)))
-            if spec.zone_axis_range is not None:
-                axes = (float(rng.uniform(*spec.zone_axis_range)),
-                        float(rng.uniform(*spec.zone_axis_range)))
-            else:
-                axes = z.semi_axes
-            er = spec.effect_range(ztype)
-            if ztype == "bush":
-                effect = 0.0
-            elif er is not None:
-                effect = float(rng.uniform(*er))
-            elif ztype == z.type:
-                effect = z.effect
-            else:
-                lo, hi = LAVA_DAMAGE_RANGE if ztype == "lava" else SWAMP_MULT_RANGE
-                effect = float(rng.uniform(lo, hi))
-            out.zones[i] = Zone(ztype, center, axes, effect)
-    if "heuristic" in spec.categories:
-        out.teams = tuple(_redraw_team(t, spec, rng) for t in out.teams)
-    return out
-
-
-def _redraw_team(t: Team, spec: LevelGenSpec, rng) -> Team:
-    if t.controller != "heuristic" or not t.has_heuristic:
-        return t
-    eps, agg = t.epsilon, t.aggressive_threshold
-    if spec.epsilon_range is not None:
-        eps = float(rng.uniform(*spec.epsilon_range))
-    if spec.aggressive_range is not None:
-        agg = float(rng.uniform(*spec.aggressive_range))
-    return replace(t, epsilon=eps, aggressive_threshold=agg)
-
-
-def mutate_level(config: Scenario, op: str, rng: np.random.Generator,
-                 spec: LevelGenSpec | None = None, delta: float = 0.1) -> Scenario:
-    """One mutation: noise on all free parameters, or a single zone edit."""
-    if op not in MUTATION_OPS:
-        raise ValueError(f"unknown mutation op {op!r}; expected one of {MUTATION_OPS}")
-    if spec is None:
-        spec = default_level_spec(config)
-    out = _copy(config)
-    if op == "perturb":
-        def bump(value: float, lo: float, hi: float) -> float:
-            width = hi - lo
-            nudged = value + float(rng.uniform(-delta * width, delta * width))
-            return float(min(max(nudged, lo), hi))
-
-        if "unit_spec" in spec.categories:
-            for i, u in enumerate(out.units):
-                nudged = {name: bump(_unit_value(u, name), lo, hi)
-                          for name, (lo, hi) in spec.unit_ranges}
-                out.units[i] = _with_unit_fields(u, nudged)
-        if "zones" in spec.categories:
-            (x0, x1), (y0, y1) = spec.center_box()
-            for i, z in enumerate(out.zones):
-                cx = bump(z.center[0], x0, x1)
-                cy = bump(z.center[1], y0, y1)
-                if spec.zone_axis_range is not None:
-                    lo, hi = spec.zone_axis_range
-                    axes = (bump(z.semi_axes[0], lo, hi), bump(z.semi_axes[1], lo, hi))
-                else:
-                    axes = z.semi_axes
-                er = spec.effect_range(z.type)
-                effect = bump(z.effect, *er) if er is not None else z.effect
-                out.zones[i] = Zone(z.type, (cx, cy), axes, effect)
-        if "heuristic" in spec.categories:
-            teams = []
-            for t in out.teams:
-                if t.controller == "heuristic" and t.has_heuristic:
-                    eps, agg = t.epsilon, t.aggressive_threshold
-                    if spec.epsilon_range is not None:
-                        eps = bump(eps, *spec.epsilon_range)
-                    if spec.aggressive_range is not None:
-                        agg = bump(agg, *spec.aggressive_range)
-                    t = replace(t, epsilon=eps, aggressive_threshold=agg)
-                teams.append(t)
-            out.teams = tuple(teams)
-        return out
-    if not out.zones:
-        return out
-    idx = int(rng.integers(len(out.zones)))
-    z = out.zones[idx]
-    if op == "swap_axes":
-        out.zones[idx] = replace(z, semi_axes=(z.semi_axes[1], z.semi_axes[0]))
-    else:
-        new_type = str(rng.choice(spec.zone_types))
-        if new_type == "bush":
-            effect = 0.0
-        else:
-            er = spec.effect_range(new_type)
-            if er is None:
-                er = LAVA_DAMAGE_RANGE if new_type == "lava" else SWAMP_MULT_RANGE
-            effect = float(rng.uniform(*er))
-        out.zones[idx] = replace(z, type=new_type, effect=effect)
-    return out
-
+    @classmethod
+    def broad(cls, base: Scenario) -> "LevelRanges":
+        """Every category open with the reference's default ranges
+        (``default_level_spec``, scenario.py:666-679)."""
+        return cls(base, units={"max_health": (20.0, 800.0), "speed": (0.5, 1.5),
+                                "attack_damage": (-10.0, 80.0)},
+                   zone_axes=(1.5, 6.0), zone_effects={"lava": (2.0, 10.0), "swamp": (0.2, 0.8)},
+                   epsilon=(0.0, 1.0), aggressive=(0.0, 0.7))
 
 # ------------------------------------------------------------- device batch --
 
@@ -256,35 +108,34 @@ _ZONE_CODE = {"lava": 1, "bush": 2, "swamp": 3}
 _M64 = (1 << 64) - 1
 
 
-def level_spec_struct(spec: LevelGenSpec):
-    """The tabx_level_spec of a LevelGenSpec (include/tabx.h)."""
+def level_spec_struct(r: LevelRanges):
+    """The tabx_level_spec of resolved ranges (include/tabx.h)."""
     from . import _native as nat
     s = nat.TabxLevelSpec()
-    s.open_units = int("unit_spec" in spec.categories)
-    s.open_zones = int("zones" in spec.categories)
-    s.open_heuristic = int("heuristic" in spec.categories)
-    ranges = dict(spec.unit_ranges)
-    for f, name in enumerate(UNIT_FREE_FIELDS):  # sorted-name order
-        if name in ranges:
+    s.open_units = int("unit_spec" in r.open)
+    s.open_zones = int("zones" in r.open)
+    s.open_heuristic = int("heuristic" in r.open)
+    for f, name in enumerate(UNIT_FIELDS):
+        if name in r.units:
             s.unit_open[f] = 1
-            s.unit_lo[f], s.unit_hi[f] = ranges[name]
-    s.n_zone_types = len(spec.zone_types)
-    for k, t in enumerate(spec.zone_types):
+            s.unit_lo[f], s.unit_hi[f] = r.units[name]
+    s.n_zone_types = len(r.zone_types)
+    for k, t in enumerate(r.zone_types):
         s.zone_types[k] = _ZONE_CODE[t]
-    (s.box_x0, s.box_x1), (s.box_y0, s.box_y1) = spec.center_box()
-    if spec.zone_axis_range is not None:
+    (s.box_x0, s.box_x1), (s.box_y0, s.box_y1) = r.center_box
+    if r.zone_axes is not None:
         s.axis_open = 1
-        s.axis_lo, s.axis_hi = spec.zone_axis_range
-    for name, (lo, hi) in spec.zone_effect_ranges:
+        s.axis_lo, s.axis_hi = r.zone_axes
+    for name, (lo, hi) in r.zone_effects.items():
         c = _ZONE_CODE[name]
         s.effect_open[c] = 1
         s.effect_lo[c], s.effect_hi[c] = lo, hi
-    if spec.epsilon_range is not None:
+    if r.epsilon is not None:
         s.eps_open = 1
-        s.eps_lo, s.eps_hi = spec.epsilon_range
-    if spec.aggressive_range is not None:
+        s.eps_lo, s.eps_hi = r.epsilon
+    if r.aggressive is not None:
         s.agg_open = 1
-        s.agg_lo, s.agg_hi = spec.aggressive_range
+        s.agg_lo, s.agg_hi = r.aggressive
     return s
 
 
@@ -313,7 +164,7 @@ def set_pcg_states(gens, packed: np.ndarray) -> None:
 
 
 class DeviceLevels:
-    """sample_level / mutate_level for a batch of levels on the device.
+    """The reference's sample_level / mutate_level for a batch of levels on the device.
 
     Levels live in the rows of ``sim``'s config table; ``sample`` and
     ``mutate`` write rows with one warp per level (``tabx_levels``) and
@@ -346,7 +197,7 @@ class DeviceLevels:
         nat.check(L.tabx_get_config(self.sim.handle, int(slot), ct.byref(c)), "tabx_get_config")
         return c
 
-    def _run(self, op: int, spec: LevelGenSpec, gens, src, dst_first, delta: float):
+    def _run(self, op: int, spec: LevelRanges, gens, src, dst_first, delta: float):
         import torch
         nat, L = self._lib()
         count = len(gens)
@@ -362,22 +213,25 @@ class DeviceLevels:
             src_t = torch.as_tensor(np.broadcast_to(np.asarray(src, np.int32), (count,)).copy(),
                                     device=dev)
         sp = level_spec_struct(spec)
+        self.sim._consume(rng_t, src_t)
         with torch.cuda.device(dev):
             nat.check(L.tabx_levels(self.sim.handle, op, ct.byref(sp), float(delta),
                                     None if src_t is None else ct.c_void_p(src_t.data_ptr()),
                                     int(dst_first), count, ct.c_void_p(rng_t.data_ptr())),
                       "tabx_levels")
+        self.sim._publish()  # the generator states are read back on this stream
         set_pcg_states(gens, rng_t.cpu().numpy().view(np.uint64))
         return list(range(dst_first, dst_first + count))
 
-    def sample(self, spec: LevelGenSpec, gens, base_slot=0, dst_first=None) -> list[int]:
-        """Row per generator: sample_level(spec, g) over the base row(s)."""
+    def sample(self, spec: LevelRanges, gens, base_slot=0, dst_first=None) -> list[int]:
+        """Row per generator: a level sampled from ``spec`` over the base row(s)
+        (scenario.py:696-747)."""
         return self._run(nat_op("sample"), spec, gens, base_slot, dst_first, 0.0)
 
-    def mutate(self, op: str, gens, slots, spec: LevelGenSpec, delta: float = 0.1,
+    def mutate(self, op: str, gens, slots, spec: LevelRanges, delta: float = 0.1,
                dst_first=None) -> list[int]:
-        """Row per generator: mutate_level(row slots[k], op, g, spec, delta);
-        ``slots=None`` mutates rows dst_first.. in place."""
+        """Row per generator: row ``slots[k]`` mutated by ``op``
+        (scenario.py:753-826); ``slots=None`` mutates rows dst_first.. in place."""
         if op not in MUTATION_OPS:
             raise ValueError(f"unknown mutation op {op!r}; expected one of {MUTATION_OPS}")
         return self._run(nat_op(op), spec, gens, slots, dst_first, delta)
@@ -393,11 +247,14 @@ class DeviceLevels:
         seeds_t = None if seeds is None else torch.as_tensor(
             np.asarray(seeds, np.uint64).view(np.int64), device=dev)
         p = lambda t: None if t is None else ct.c_void_p(t.data_ptr())  # noqa: E731
+        self.sim._consume(lanes_t, slots_t, seeds_t)
         with torch.cuda.device(dev):
             nat.check(L.tabx_respawn_lanes(self.sim.handle, p(lanes_t), p(slots_t), p(seeds_t),
                                            lanes_t.numel()), "tabx_respawn_lanes")
+        if slots is not None:
+            self.sim.lane_slots[np.asarray(lanes, np.int64)] = np.asarray(slots, np.int32)
         self.sim._init_output()
-        torch.cuda.current_stream(dev).synchronize()
+        self.sim._stream.synchronize()
 
 
 def nat_op(name: str) -> int:

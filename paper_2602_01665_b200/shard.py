@@ -21,7 +21,7 @@ import numpy as np
 from .rng import lane_seeds
 
 STAT_KEYS = ("episodes", "ally_wins", "first_kill_ally", "truncation_ties", "sum_length",
-             "sum_return", "eliminations")
+             "sum_return", "eliminations", "env_steps")
 
 
 def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
@@ -69,10 +69,13 @@ def summarize(stats: dict) -> dict:
 
 
 def stats_from_outputs(done, winner, reason, first_kill, episode_length,
-                       episode_return) -> dict:
-    """Statistics of the lanes that finished on one step (host arrays)."""
+                       episode_return, running=None) -> dict:
+    """Statistics of one step (host arrays): the lanes that finished, and the
+    env-steps taken (``running``: lanes that were running; default all, as
+    under auto-reset)."""
     d = np.asarray(done, bool)
     return {
+        "env_steps": float(d.size if running is None else np.count_nonzero(running)),
         "episodes": float(d.sum()),
         "ally_wins": float((np.asarray(winner)[d] == 0).sum()),
         "first_kill_ally": float((np.asarray(first_kill)[d] == 0).sum()),

@@ -133,18 +133,28 @@ class BatchSim:
                     f"got ({c.max_units}, {c.max_zones}) vs ({self.n_units}, {self.n_zones})")
         self.obs_dim = int(L.tabx_obs_dim(self.n_units, self.n_zones))
         self.global_dim = int(L.tabx_global_dim(self.n_units, self.n_zones))
-        # distinct configs -> table
-        self._cfg_index: dict[int, int] = {}
+        # distinct configs (by content: equal templates share a slot) -> table
+        built: dict[int, int] = {}
+        by_bytes: dict[bytes, int] = {}
         table = []
         lane_cfg = np.zeros(self.batch, np.int32)
         for b, c in enumerate(configs):
-            if id(c) not in self._cfg_index:
-                self._cfg_index[id(c)] = len(table)
-                table.append(build_config(c, validate=False))
-            lane_cfg[b] = self._cfg_index[id(c)]
+            k = built.get(id(c))
+            if k is None:
+                row = build_config(c, validate=False)
+                k = by_bytes.setdefault(bytes(row), len(table))
+                if k == len(table):
+                    table.append(row)
+                built[id(c)] = k
+            lane_cfg[b] = k
+        # the config-table slot every lane runs on (the C side's mirror)
+        self.lane_slots = lane_cfg.copy()
         arr = (nat.TabxConfig * len(table))(*table)
         seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(self.batch))
         self._stream = stream or torch.cuda.current_stream(self.device)
+        # a caller-given stream other than the current one needs cross-stream
+        # ordering on every call (see _consume / _publish)
+        self._side_stream = stream is not None
         h = ct.c_void_p()
         with torch.cuda.device(self.device):
             nat.check(L.tabx_create(arr, len(table), lane_cfg.ctypes.data_as(ct.c_void_p),
@@ -205,21 +215,53 @@ class BatchSim:
 
     def _init_output(self) -> None:
         L = nat.lib()
+        if self._side_stream:
+            self._consume()
         with torch.cuda.device(self.device):
             nat.check(L.tabx_init_output(self._h, ct.byref(self._outs)), "tabx_init_output")
+        if self._side_stream:
+            self._publish()
         self.last = self._output()
 
+    # ------------------------------------------------------------ streams --
+    # Inputs are produced on torch's current stream and the kernels run on
+    # the simulator's stream: order the two before each launch, and tell the
+    # caching allocator the simulator's stream reads the input.
+    def _consume(self, *tensors) -> None:
+        if not self._side_stream:
+            return
+        cur = torch.cuda.current_stream(self.device)
+        if cur != self._stream:
+            self._stream.wait_stream(cur)
+            for t in tensors:
+                if t is not None and t.is_cuda:
+                    t.record_stream(self._stream)
+
+    def _publish(self) -> None:
+        """Make torch's current stream see the simulator stream's writes."""
+        if not self._side_stream:
+            return
+        cur = torch.cuda.current_stream(self.device)
+        if cur != self._stream:
+            cur.wait_stream(self._stream)
+
     # ---------------------------------------------------------------- api --
-    def step(self, actions=None) -> BatchOutput:
+    def step(self, actions=None, strict: bool | None = None) -> BatchOutput:
+        """One step of every lane; ``strict`` (default: the simulator's)
+        raises a latched ActionMaskError synchronously."""
         act_t = None
         if actions is not None:
             act_t = self._actions_tensor(actions)
+        if self._side_stream:
+            self._consume(act_t)
         # (the C side selects the handle's device for its launches)
         rc = self._step_fn(self._h, _ptr(act_t), self._outs_ref)
         if rc:
             nat.check(rc, "tabx_step")
         self._keep_actions = act_t  # keep alive until the stream consumed it
-        if act_t is not None and self.strict:
+        if self._side_stream:
+            self._publish()
+        if act_t is not None and (self.strict if strict is None else strict):
             self.check_errors()
         self.last = self._output()
         return self.last
@@ -249,27 +291,53 @@ class BatchSim:
             raise ActionMaskError(f"invalid action {err.action} for unit {err.unit} in env {err.env}")
 
     def reset_env(self, b: int, config: Scenario | None = None, seed: int | None = None) -> None:
+        """Restart lane ``b`` (environment.py:490-498).  Asynchronous: a new
+        config's row is staged and uploaded on the stream; the lane's slot
+        (shared with equal configs, recycled once no lane uses it) is kept in
+        ``lane_slots``."""
         L = nat.lib()
         if not 0 <= b < self.batch:
             raise IndexError(f"env {b} out of range")
         cfg_ptr = None
         if config is not None:
             ensure_valid(config)
-            self.configs[b] = config
             cfg = build_config(config, validate=False)
             cfg_ptr = ct.byref(cfg)
+        slot = ct.c_int32(-1)
+        if self._side_stream:
+            self._consume()
         with torch.cuda.device(self.device):
             nat.check(L.tabx_reset_env(self._h, int(b), cfg_ptr,
                                        ct.c_uint64(0 if seed is None else int(seed) & (2**64 - 1)),
-                                       0 if seed is None else 1, ct.byref(self._outs)),
+                                       0 if seed is None else 1, ct.byref(self._outs),
+                                       ct.byref(slot)),
                       "tabx_reset_env")
+        if config is not None:
+            self.configs[b] = config
+        self.lane_slots[b] = slot.value
+        if self._side_stream:
+            self._publish()
         self.last = self._output()
+
+    def config_slot_info(self, slot: int) -> tuple[int, bool]:
+        """(lanes on ``slot``, pinned) as tracked by the C side."""
+        lanes, pinned = ct.c_int64(), ct.c_int32()
+        nat.check(nat.lib().tabx_config_slot(self._h, int(slot), ct.byref(lanes),
+                                             ct.byref(pinned)), "tabx_config_slot")
+        return lanes.value, bool(pinned.value)
+
+    def num_configs(self) -> tuple[int, int]:
+        """(rows, capacity) of the handle's config table."""
+        n, cap = ct.c_int32(), ct.c_int32()
+        nat.check(nat.lib().tabx_num_configs(self._h, ct.byref(n), ct.byref(cap)),
+                  "tabx_num_configs")
+        return n.value, cap.value
 
     def respawn_all(self, seeds) -> None:
         """Fresh episodes for every lane with new seeds (bindings reset)."""
         L = nat.lib()
         seeds = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(self.batch))
-        lane_cfg = np.array([self._cfg_index.get(id(c), 0) for c in self.configs], np.int32)
+        lane_cfg = np.ascontiguousarray(self.lane_slots, dtype=np.int32)
         with torch.cuda.device(self.device):
             nat.check(L.tabx_respawn_all(self._h, seeds.ctypes.data_as(ct.c_void_p),
                                          lane_cfg.ctypes.data_as(ct.c_void_p)),
@@ -285,9 +353,11 @@ class BatchSim:
             shape = (B,) if k in PER_LANE else (B, N) + tuple(N if x == "N" else x for x in tail)
             out[k] = torch.empty(shape, dtype=dt, device=self.device)
         st = nat.TabxState(*[_ptr(out[k]) for k in nat.STATE_FIELDS])
+        if self._side_stream:
+            self._consume()
         with torch.cuda.device(self.device):
             nat.check(L.tabx_export_state(self._h, ct.byref(st)), "tabx_export_state")
-        torch.cuda.current_stream(self.device).synchronize()
+        self._stream.synchronize()
         return out
 
     def export_lanes(self, lanes: torch.Tensor, fields=None) -> dict[str, torch.Tensor]:
@@ -304,9 +374,14 @@ class BatchSim:
             shape = (n,) if k in PER_LANE else (n, N) + tuple(N if x == "N" else x for x in tail)
             out[k] = torch.empty(shape, dtype=dt, device=self.device)
         st = nat.TabxState(*[_ptr(out.get(k)) for k in nat.STATE_FIELDS])
+        if self._side_stream:
+            self._consume(lanes)
         with torch.cuda.device(self.device):
             nat.check(L.tabx_export_lanes(self._h, _ptr(lanes), n, ct.byref(st)),
                       "tabx_export_lanes")
+        if self._side_stream:
+            for v in out.values():
+                v.record_stream(self._stream)
         self._keep_lanes = lanes
         return out
 
@@ -324,9 +399,13 @@ class BatchSim:
                 v = torch.from_numpy(np.ascontiguousarray(v))
             keep[k] = v.to(device=self.device, dtype=dt).contiguous()
         st = nat.TabxState(*[_ptr(keep.get(k)) for k in nat.STATE_FIELDS])
+        if self._side_stream:
+            self._consume(*keep.values())
         with torch.cuda.device(self.device):
             nat.check(L.tabx_import_state(self._h, ct.byref(st)), "tabx_import_state")
-        torch.cuda.current_stream(self.device).synchronize()
+        self._stream.synchronize()
+        if "config" in keep:
+            self.lane_slots = keep["config"].cpu().numpy().astype(np.int32)
 
     def episode_stats(self, reset: bool = False, device_out: torch.Tensor | None = None) -> dict:
         """Per-shard episode statistics (rollout.summarize inputs)."""

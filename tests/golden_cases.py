@@ -108,6 +108,11 @@ CASES = {
                (("units", 1, "heading_deg"), -75.0),
                (("units", 2, "position"), [0.0, 40.0])],
         resets={60: [(0, 101), (3, 103)], 61: [(1, 102)], 121: [(2, 104), (4, 105)]}),
+    # N = 150 on terrain: the W = 8 path (5 words per cache row) and
+    # numpy's recursive pairwise split (n > 128) in the team-health sums;
+    # short episodes so truncations, ties / wins and auto-resets all occur.
+    "w8_terrain": dict(scenario="c6_75v75_terrain", batch=3, steps=45, auto_reset=True,
+                       run_seed=12, edits=[(("max_steps",), 20)]),
     # Two units spawned on the same point (coincident-centre contact normal),
     # random vs random.
     "coincident": dict(scenario="mixed_kings", batch=3, steps=40, auto_reset=True,

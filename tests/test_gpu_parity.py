@@ -95,7 +95,8 @@ def _perturbed_states(sc, B, seed):
 
 @pytest.mark.parametrize("scen,B,seed", [("c3_10v10_terrain", 96, 1), ("c2_10v10", 64, 2),
                                          ("mixed_kings", 128, 3), ("duel_terrain", 256, 4),
-                                         ("c4_50v50", 6, 5), ("c1_3v3", 256, 6)])
+                                         ("c4_50v50", 6, 5), ("c1_3v3", 256, 6),
+                                         ("c6_75v75_terrain", 6, 11)])
 def test_injected_state_single_step(scen, B, seed):
     sc = builtin_scenario(scen).with_controllers(ally="random", enemy="heuristic:medium")
     ora = _perturbed_states(sc, B, seed)
@@ -489,3 +490,23 @@ def test_shape_specialised_kernels_equal_generic(scen, B, monkeypatch):
     s0, s1 = (s.export_state() for s in sims)
     for k in ("pos", "health", "heading", "alive", "mem_pos", "vis", "atk"):
         assert torch.equal(s0[k], s1[k]), k
+
+
+def test_misaligned_global_state_is_rejected_before_launch():
+    """global_state leaves through TMA bulk stores: a buffer that is not
+    16-byte aligned is refused with TABX_E_ALIGNMENT (no launch, the context
+    stays healthy)."""
+    import ctypes as ct
+
+    from paper_2602_01665_b200 import _native as nat
+    sc = builtin_scenario("c1_3v3").scripted()
+    gpu = BatchSim([sc] * 4, np.arange(4, dtype=np.uint64), device="cuda:0")
+    raw = torch.empty(4 * gpu.global_dim + 1, dtype=torch.float32, device="cuda:0")
+    outs = nat.TabxOutputs.from_buffer_copy(gpu._outs)
+    outs.global_state = raw.data_ptr() + 4
+    rc = nat.lib().tabx_step(gpu.handle, None, ct.byref(outs))
+    assert rc == nat.E_ALIGNMENT
+    assert "16-byte" in nat.lib().tabx_last_error().decode()
+    gpu.step(None)
+    torch.cuda.synchronize()
+    gpu.close()

@@ -1,6 +1,6 @@
-"""Level sampling / mutation, host mirror.
+"""Level sampling / mutation, host restatement.
 
-``paper_2602_01665_b200.levels`` must reproduce the reference generator draw
+``oracle/levels_oracle.py`` (the checker of the device batch) must reproduce the reference generator draw
 for draw: the canonical JSON of every level and the numpy generator state
 after every call equal ``tests/golden/levels.json`` (``tools/make_levels.py``
 over ``pkg/src/skirmish/scenario.py:696-826``).  Spec validation follows
@@ -16,7 +16,8 @@ import os
 import numpy as np
 import pytest
 
-from paper_2602_01665_b200 import levels
+import harness  # noqa: F401  (puts oracle/ on sys.path)
+import levels_oracle as levels
 from paper_2602_01665_b200.scenario import load_scenario, save_scenario
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "levels.json")
@@ -99,3 +100,33 @@ def test_closed_spec_and_zero_delta_keep_the_base():
     for ub, um in zip(base.units, out.units):
         assert um.resolved_spec() == ub.resolved_spec()
     assert out.zones == base.zones and out.teams == base.teams
+
+
+def test_device_ranges_resolve_like_the_reference_spec():
+    """The product's LevelRanges (what DeviceLevels reads) resolves every
+    range exactly as the reference's LevelGenSpec does, and rejects the same
+    inputs (scenario.py:581-663)."""
+    from paper_2602_01665_b200.levels import LevelRanges, level_spec_struct
+    base = load_scenario(CASES["duel_default_samples"]["base"])
+    for bad in (dict(open=("units",)), dict(units={"body_mass": (1, 2)}),
+                dict(zone_effects={"bush": (0.0, 1.0)}), dict(units={"speed": (2.0, 1.0)}),
+                dict(zone_types=("mud",))):
+        with pytest.raises(ValueError):
+            LevelRanges(base, **bad)
+    r = LevelRanges(base, units={"max_health": (-50.0, 900.0)}, zone_effects={"swamp": (0.0, 3.0)},
+                    epsilon=(-1.0, 2.0), zone_axes=(-1.0, 0.05), aggressive=(-2.0, 0.5))
+    h = levels.LevelGenSpec(base=base, unit_ranges={"max_health": (-50.0, 900.0)},
+                            zone_effect_ranges={"swamp": (0.0, 3.0)}, epsilon_range=(-1.0, 2.0),
+                            zone_axis_range=(-1.0, 0.05), aggressive_range=(-2.0, 0.5))
+    assert r.units == dict(h.unit_ranges)
+    assert r.zone_effects == dict(h.zone_effect_ranges)
+    assert (r.epsilon, r.zone_axes, r.aggressive) == (h.epsilon_range, h.zone_axis_range,
+                                                      h.aggressive_range)
+    assert r.center_box == h.center_box() == ((2.0, 38.0), (2.0, 38.0))
+    b, d = LevelRanges.broad(base), levels.default_level_spec(base)
+    assert b.units == dict(d.unit_ranges) and b.zone_effects == dict(d.zone_effect_ranges)
+    assert (b.epsilon, b.zone_axes, b.aggressive) == (d.epsilon_range, d.zone_axis_range,
+                                                      d.aggressive_range)
+    s = level_spec_struct(b)
+    assert (s.open_units, s.open_zones, s.open_heuristic, s.n_zone_types) == (1, 1, 1, 3)
+    assert list(s.unit_open) == [1, 1, 1] and (s.unit_lo[1], s.unit_hi[1]) == (20.0, 800.0)

@@ -27,6 +27,9 @@ SCENARIOS = {
     # small extra shapes used by parity tests
     "duel_terrain": "1F1Avs1S1H_2L2B2S",
     "mixed_kings": "2F1M2Avs2S1K",
+    # 150 units (five visibility words, the W = 8 kernels; team-health sums
+    # past numpy's 128-element pairwise block) on terrain
+    "c6_75v75_terrain": "20F10S20A10D10H5Pvs20F10S20A10D10H5P_2L2B2S",
 }
 
 
