@@ -404,39 +404,54 @@ def measure_e2e(cx: Ctx, key: str, per: int, steps: int, warmup: int, seed: int)
 
 
 def measure_host_obs(cx: Ctx, key: str, per: int, steps: int, seed: int) -> dict:
-    """What a host-side consumer of the reference's numpy outputs pays: every
-    step's float32 observations copied to pinned host memory (PCIe bound)."""
+    """What a host-side consumer of the reference's numpy outputs pays: each
+    step's host actions uploaded, then the float32 observations and the
+    action mask copied back to pinned host memory (PCIe bound), with the
+    strict (synchronous) action check of bindings.step."""
+    import numpy as np
+
     from paper_2602_01665_b200 import bindings, shard
     from paper_2602_01665_b200.scenario import builtin_scenario, save_scenario
 
     torch = cx.torch
     total = per * cx.world
     first, _ = shard.shard_range(total, cx.world, cx.rank)
-    base = builtin_scenario(SCENARIOS[key])
-    h = bindings.make_batch(save_scenario(base.scripted()).encode(), per, seed, device=cx.dev,
+    base = builtin_scenario(SCENARIOS[key])  # ally external, enemy heuristic-medium
+    N = base.max_units
+    h = bindings.make_batch(save_scenario(base).encode(), per, seed, device=cx.dev,
                             first_lane=first, interactions=False, final_observations=False)
     obs = h.sim.last.observations
     host = torch.empty(obs.shape, dtype=obs.dtype).pin_memory()
     mask_host = torch.empty(h.sim.last.action_mask.shape, dtype=torch.bool).pin_memory()
-    bindings.step(h, None)
+    gen = np.random.default_rng(99 + cx.rank)
+    act_host = torch.from_numpy(gen.integers(0, 5, size=(per, N), dtype=np.int64)).pin_memory()
+    act_dev = torch.empty_like(act_host, device=cx.dev)
+
+    def one():
+        act_dev.copy_(act_host, non_blocking=True)
+        out = bindings.step(h, act_dev)
+        host.copy_(out[0], non_blocking=True)
+        mask_host.copy_(out[5], non_blocking=True)
+
+    one()
     cx.barrier()
     e0, e1 = cx.event(), cx.event()
     e0.record(cx.stream)
     for _ in range(steps):
-        out = bindings.step(h, None)
-        host.copy_(out[0], non_blocking=True)
-        mask_host.copy_(out[5], non_blocking=True)
+        one()
     e1.record(cx.stream)
     cx.barrier()
     ms = cx.max_over_ranks(e0.elapsed_time(e1))
     h.sim.close()
     del h, host, mask_host
     torch.cuda.empty_cache()
+    D = obs.shape[2]
     return {"value": total * steps / (ms / 1000.0), "unit": "env-steps/s", "steps": steps,
-            "d2h_bytes_per_step": per * (obs.shape[1] * obs.shape[2] * 4 + obs.shape[1] * 7),
-            "note": "bindings.step + observations and action mask copied to pinned host "
-                    "memory every step (the reference's step returns numpy arrays); bound by "
-                    "the PCIe device-to-host link"}
+            "h2d_bytes_per_step": per * N * 8,
+            "d2h_bytes_per_step": per * N * (4 * D + 7),
+            "note": "host int64 actions in, float32 observations + action mask out to pinned "
+                    "host memory every step (the reference's bindings.step returns numpy "
+                    "arrays); bound by the PCIe device-to-host link"}
 
 
 def measure_reconfig(cx: Ctx, batches=(8, 262144)) -> dict:

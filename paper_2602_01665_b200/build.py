@@ -99,5 +99,25 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return OUT
 
 
+CHECKED_OUT = os.path.join(HERE, "_tabx_checked.so")
+
+
+def build_checked(verbose: bool = False) -> str:
+    """The checked variant (-DTABX_CHECKS: device asserts, shared memory
+    poisoned per environment, per-lane random delays at phase boundaries),
+    a test-only library loaded with TABX_LIB by tests/test_gpu_checked.py."""
+    global OUT, FLAGS
+    saved = OUT, FLAGS
+    OUT = CHECKED_OUT
+    FLAGS = ["-DTABX_CHECKS"] + FLAGS
+    try:
+        return build(verbose=verbose)
+    finally:
+        OUT, FLAGS = saved
+
+
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    if "--checked" in sys.argv:
+        print(build_checked(verbose="-v" in sys.argv))
+    else:
+        print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

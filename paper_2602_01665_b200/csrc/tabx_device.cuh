@@ -8,6 +8,49 @@
 
 namespace tabx {
 
+// ---- checked build (-DTABX_CHECKS; test infrastructure):
+// device asserts on indices and store ranges, per-lane random delays at
+// the step's phase boundaries (a shared-memory hand-off missing its
+// __syncwarp / __syncthreads then reads a stale value, which the bit-exact
+// parity tests see), and shared memory poisoned before each environment
+// (a read of a value this environment never wrote is a NaN / garbage).
+#ifdef TABX_CHECKS
+#include <stdio.h>
+#define TABX_ASSERT(c)                                                             \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("TABX_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                   \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+__device__ __forceinline__ void tabx_jitter(unsigned k) {
+  unsigned x = (unsigned)clock() ^ (threadIdx.x * 0x9E3779B9u) ^ (blockIdx.x * 0x85EBCA6Bu) ^
+               (k * 0xC2B2AE35u);
+  x ^= x >> 15;
+  x *= 0x2C1B3C6Du;
+  x ^= x >> 12;
+  __nanosleep(x & 1023u);
+}
+#define TABX_JITTER(k) ::tabx::tabx_jitter(k)
+// fill [p, p + bytes) with 0xFF bytes (float NaN, int -1) from `n` threads
+__device__ __forceinline__ void tabx_poison(void* p, size_t bytes, int t, int n) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(p);
+  for (size_t q = t; q < bytes / 4; q += n) w[q] = 0xFFFFFFFFu;
+}
+#define TABX_POISON(p, bytes, t, n) ::tabx::tabx_poison(p, bytes, t, n)
+#else
+#define TABX_ASSERT(c) \
+  do {                 \
+  } while (0)
+#define TABX_JITTER(k) \
+  do {                 \
+  } while (0)
+#define TABX_POISON(p, bytes, t, n) \
+  do {                              \
+  } while (0)
+#endif
+
 constexpr int A_ROTATE = 4;
 constexpr int A_ATTACK = 5;
 constexpr int A_NOOP = 6;

@@ -100,6 +100,11 @@ __device__ __forceinline__ void load_view(const EmitScratch<W>& X, const DevStat
                                           int N, int Z, const tabx_config* __restrict__ C,
                                           const DerivedCfg* __restrict__ DC, int lane) {
   const EmitEnv<W>& E = X.E;
+  // (checked build) the view and pair list, not the stage buffers a bulk
+  // store may still be reading
+  TABX_POISON(X.E.px, (size_t)((const unsigned char*)X.stage - (const unsigned char*)X.E.px),
+              lane, 32);
+  __syncwarp();
   for (int u = lane; u < N; u += 32) {
     const int64_t gu = b * N + u;
     const double2 p = st.pos[gu];
@@ -125,6 +130,7 @@ __device__ __forceinline__ void load_view(const EmitScratch<W>& X, const DevStat
       const int v = __shfl_up_sync(0xffffffffu, incl, d);
       if (lane >= d) incl += v;
     }
+    TABX_JITTER(300);
     if (valid) X.rstart[lane + 1] = (uint16_t)incl;
     if (lane == 0) X.rstart[0] = 0;
     for (int n = incl - c; w; w &= w - 1, ++n)
@@ -169,6 +175,7 @@ __device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs,
   const int pad = (int)(gs & 3);
   const int64_t a0 = (gs + 3) & ~(int64_t)3;
   const int64_t a1 = (gs + count) & ~(int64_t)3;
+  TABX_ASSERT(gs >= 0 && count > 0 && ((uintptr_t)(dst + a0) & 15u) == 0);
   if (a1 > a0) {
     if (lane == 0) bulk_s2g(dst + a0, stage + pad + (a0 - gs), (uint32_t)((a1 - a0) * 4));
     // <= 3 head floats on lanes 0..2, <= 3 tail floats on lanes 4..6
@@ -181,6 +188,12 @@ __device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs,
   // one (possibly empty) bulk group per flush keeps the double-buffer
   // accounting exact: wait_group.read 1 frees the buffer before the last
   if (lane == 0) bulk_commit();
+}
+
+// a chunk of `count` floats starting at global float gs fits its stage
+// buffer of SF floats at the alignment pad gs & 3
+__device__ __forceinline__ bool pad_fits(int64_t gs, int count, int SF) {
+  return (int)(gs & 3) + count <= SF;
 }
 
 // Position of the n-th (0-based) set bit of w, by popc halving.
@@ -244,6 +257,8 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
     for (int r0 = 0; r0 < N; r0 += R) {
       const int nr = min(R, N - r0);
       const int64_t gs = (b * N + r0) * (int64_t)D;
+      TABX_ASSERT(nr > 0 && (pad_fits(gs, nr * D, SF)));
+      TABX_JITTER(301);
       float* st = X.stage + buf * SF;
       const int pad = (int)(gs & 3);
       float* row0 = st + pad;
@@ -265,6 +280,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
       }
       // visible pairs of the chunk's rows (vis excludes inactive rows/columns)
       auto pair_block = [&](int r, int j) {
+        TABX_ASSERT(r >= r0 && r < r0 + nr && j >= 0 && j < N && j != r);
         const int kk = j - (j > r ? 1 : 0);
         float* blk = row0 + (r - r0) * D + TABX_OWN_DIM + TABX_OTHER_DIM * kk;
         const float4* oj = reinterpret_cast<const float4*>(E.own[j]);
@@ -349,6 +365,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
           }
         }
       }
+      TABX_JITTER(302);
       fence_proxy_async();
       __syncwarp();
       if (obs) flush_stage(obs, gs, nr * D, st, lane);
@@ -394,6 +411,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
       row[e] = E.own[u][e - u * TABX_OWN_DIM];
     }
     for (int q = lane; q < ZD; q += 32) row[N * TABX_OWN_DIM + q] = DC->zglob[q];
+    TABX_JITTER(303);
     fence_proxy_async();
     __syncwarp();
     flush_stage(glob, gs, G, st, lane);

@@ -68,15 +68,11 @@ __device__ unsigned long long tabx_phase_cycles[16];
     ph_t0_ = ph_t1_;                                                   \
   } while (0)
 #else
-#define TABX_PHASE_DIV(k) \
-  do {                    \
-  } while (0)
+#define TABX_PHASE_DIV(k) TABX_JITTER(100 + (k))
 #define TABX_PHASE_BEGIN() \
   do {                     \
   } while (0)
-#define TABX_PHASE(k) \
-  do {                \
-  } while (0)
+#define TABX_PHASE(k) TABX_JITTER(k)
 #endif
 
 // ------------------------------------------------------------- helpers --
@@ -658,6 +654,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const bool valid = i < N;
   const int64_t u = b * N + i;
   const DevState& st = P.st;
+  TABX_ASSERT(b >= 0 && b < P.B && N <= 32 * W && Z <= TABX_MAX_ZONES && P.st.cfg[b] >= 0);
   const tabx_config* __restrict__ C = P.cfgs + st.cfg[b];
   const DerivedCfg* __restrict__ DC = P.dcfgs + st.cfg[b];
   const UnitStatic U = load_static(C, i, valid);
@@ -1010,6 +1007,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
       if (p < NP && running) {
         const uint32_t ij = S.ptab[p];
         const int a = (int)(ij >> 8), c = (int)(ij & 255u);
+        TABX_ASSERT(a < c && c < N);
         if (S.uf[a] & S.uf[c] & UF_ACTIVE) {
           const double dx = S.px[c] - S.px[a], dy = S.py[c] - S.py[a];
           const double rs = S.rad[a] + S.rad[c];
@@ -1172,6 +1170,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   // 9. combat (combat.py:86-113; environment.py:259-265)
   const bool swing = act == A_ATTACK && alive && U.active && cd <= 0.0;
   const bool landed = running && swing && tgt >= 0;
+  TABX_ASSERT(tgt >= -1 && tgt < N && act >= 0 && act < TABX_NUM_ACTIONS);
   S.tgt[i] = landed ? tgt : -1;
   env_sync<W>();
   // per-victim damage: landed attackers in ascending order (combat.py:108)
@@ -1373,6 +1372,9 @@ __global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
   for (int64_t b = (int64_t)blockIdx.x * EPB + g; work && b < P.B;
        b += (int64_t)gridDim.x * EPB) {
     if (M == MODE_RESET && !(P.st.flags[b] & F_PEND)) continue;  // env-uniform
+    // (checked build) everything but the kernel-lifetime pair table
+    TABX_POISON(&envs[g], offsetof(EnvSmem<W>, ptab), i, 32 * W);
+    env_sync<W>();
     run_lane<W, M, NF, ZF>(P, b, i, envs[g],
                 M == MODE_RESET ? view_base + g * view_bytes
                                      : nullptr,
@@ -1431,6 +1433,8 @@ __global__ void __launch_bounds__(128, TABX_K0_MINB) ctrl_kernel(const Params P,
   const int64_t stride = (int64_t)gridDim.x * wpb * G;
   const int g = lane / NH, k = lane - g * NH;
   for (int64_t b0 = ((int64_t)blockIdx.x * wpb + wib) * G; b0 < P.B; b0 += stride) {
+    TABX_POISON(V, sizeof(CtrlView<W>) * G, lane, 32);
+    __syncwarp();
     for (int q = lane; q < G * W; q += 32) {
       V[q / W].m_active[q % W] = 0u;
       V[q / W].m_alive[q % W] = 0u;
@@ -1473,6 +1477,7 @@ __global__ void __launch_bounds__(128, TABX_K0_MINB) ctrl_kernel(const Params P,
       const int nheur = (st.flags[b] & F_DONE) ? 0 : DC->n_heur;
       for (int kk = k; kk < nheur; kk += NH) {
         const int i = DC->hlist[kk];
+        TABX_ASSERT(i >= 0 && i < N);
         const int64_t u = b * N + i;
         const uint8_t ub = st.ubits[u];
         if (ub & U_ALIVE) {  // free: alive, active (hlist), lane running
@@ -1495,6 +1500,8 @@ __global__ void __launch_bounds__(128, TABX_K0_MINB) ctrl_kernel(const Params P,
           const int r = scripted_body<W>(view, C, i, N, Z, hd, cd, speff * C->dt, mask7, ue, up,
                                          C->epsilon[team], C->aggressive[team], DC->bush_m, m.x,
                                          m.y, (ub & U_MEMV) != 0);
+          TABX_ASSERT((r & SA_ACT_MASK) < TABX_NUM_ACTIONS);
+          TABX_JITTER(200);
           P.ctrl_act[u] = (int8_t)(r & SA_ACT_MASK);
           if (r & SA_HAS) {
             const int tg = r >> SA_TGT_SHIFT;
