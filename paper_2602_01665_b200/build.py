@@ -102,7 +102,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
 CHECKED_OUT = os.path.join(HERE, "_tabx_checked.so")
 
 
-def build_checked(verbose: bool = False) -> str:
+def build_checked(verbose: bool = False, selftest: bool = False) -> str:
     """The checked variant (-DTABX_CHECKS: device asserts, shared memory
     poisoned per environment, per-lane random delays at phase boundaries),
     a test-only library loaded with TABX_LIB by tests/test_gpu_checked.py."""
@@ -110,6 +110,9 @@ def build_checked(verbose: bool = False) -> str:
     saved = OUT, FLAGS
     OUT = CHECKED_OUT
     FLAGS = ["-DTABX_CHECKS"] + FLAGS
+    if selftest:  # negative control: one stage hand-off without its __syncwarp
+        OUT = os.path.join(HERE, "_tabx_selftest_race.so")
+        FLAGS = ["-DTABX_SELFTEST_RACE"] + FLAGS
     try:
         return build(verbose=verbose)
     finally:
@@ -117,7 +120,7 @@ def build_checked(verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    if "--checked" in sys.argv:
-        print(build_checked(verbose="-v" in sys.argv))
+    if "--checked" in sys.argv or "--selftest" in sys.argv:
+        print(build_checked(verbose="-v" in sys.argv, selftest="--selftest" in sys.argv))
     else:
         print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))

@@ -987,6 +987,9 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   env_sync<W>();
   S.px[i] = px;
   S.py[i] = py;
+#ifdef TABX_SELFTEST_RACE  // negative control of the checked build: W > 1 hand-off without its barrier
+  if (W == 1)
+#endif
   env_sync<W>();
 
   // 5. contacts: detection (physics.py:27-49), Gauss-Seidel (physics.py:52-94)
