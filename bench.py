@@ -282,7 +282,8 @@ def measure_device(cx: Ctx, key: str, per: int, steps: int, warmup: int, seed: i
            "ms_per_step": elapsed_ms / steps, "steps": steps, "warmup": warmup,
            "agent_steps_per_s": total * steps / (elapsed_ms / 1000.0) * len(sc.units),
            "envs": total, "envs_per_gpu": per, "n_units": N, "n_zones": Z,
-           "clocks": clk.summary(), "gpu_launches": launches_per_step(per) * steps}
+           "clocks": clk.summary(), "step_path": sim.step_path(),
+           "gpu_launches": (launches_per_step(per) - (sim.step_path() == "fused")) * steps}
     if profile:
         # per-kernel times (roofline) from a second pass of the same length with
         # CUDA events around every kernel, so their host cost stays out of `value`
@@ -318,17 +319,27 @@ def roofline(key: str, N: int, Z: int, per: int, kern_ms: float, kprof: dict) ->
     obs_bytes = 4 * N * D + 4 * G + 57 * N + 5  # writes + the per-unit view it reads
     step_bytes = bytes_per - (4 * N * D + 4 * G)
     kernels = []
-    for name, ms, nbytes in (("step_kernels (K0 heuristic-controller pass + K1 actions..rewards, "
-                              "caches, state)", kprof["step_kernel_ms"], step_bytes),
-                             ("obs_kernel (K2: observation + global-state stream, TMA)",
-                              kprof["obs_kernel_ms"], obs_bytes),
-                             ("reset_kernel (K3: deferred auto-resets)",
-                              kprof["reset_kernel_ms"], None)):
+    if kprof.get("fused"):
+        # refresh check + K0 (re-reads of the unit view only), then one fused
+        # kernel: the step's state traffic + the observation stream
+        rows = (("ctrl_kernels (refresh check + K0 heuristic-controller pass)",
+                 kprof["ctrl_kernel_ms"], None),
+                ("fused_kernel (K1 actions..rewards, caches, state + K2 observation and "
+                 "global-state stream, TMA; warp-specialised)", kprof["fused_kernel_ms"],
+                 step_bytes + obs_bytes),
+                ("reset_kernel (K3: deferred auto-resets)", kprof["reset_kernel_ms"], None))
+    else:
+        rows = (("step_kernels (K0 heuristic-controller pass + K1 actions..rewards, "
+                 "caches, state)", kprof["step_kernel_ms"], step_bytes),
+                ("obs_kernel (K2: observation + global-state stream, TMA)",
+                 kprof["obs_kernel_ms"], obs_bytes),
+                ("reset_kernel (K3: deferred auto-resets)", kprof["reset_kernel_ms"], None))
+    for name, ms, nbytes in rows:
         ent = {"kernel": name, "ms_avg": ms}
         if nbytes and ms > 0:
             gbs = nbytes * per / (ms / 1000.0) / 1e9
             ent.update({"bytes_per_env_step": nbytes, "achieved_gbs": gbs, "frac": gbs / peak})
-        if "obs_kernel" in name and ms > 0:
+        if ("obs_kernel" in name or "fused_kernel" in name) and ms > 0:
             strict = (4 * N * D + 4 * G) * per / (ms / 1000.0) / 1e9
             ent["frac_obs_bytes_only"] = strict / peak
         kernels.append(ent)

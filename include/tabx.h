@@ -323,6 +323,15 @@ int tabx_set_profiling(tabx_handle* h, int32_t enable);
 int tabx_get_profile(tabx_handle* h, double* ms, int64_t* steps);
 
 /*
+ * Which kernels the last tabx_step ran: *fused = 1 when the fused step +
+ * observation kernel did (W = 1, heuristic-controller pass on, a shape with
+ * specialised kernels, and TABX_FUSED=1 at creation: it is off by default), 0 for the separate step
+ * and observation kernels.  With fused = 1 the profile's ms[0] covers the
+ * refresh check + controller pass and ms[1] the fused kernel.
+ */
+int tabx_step_path(const tabx_handle* h, int32_t* fused);
+
+/*
  * Config table management.  The table starts with the configs given to
  * tabx_create (plus those added by tabx_reset_env); tabx_reserve_configs
  * grows its capacity (synchronises; reallocates the table, so CUDA graphs

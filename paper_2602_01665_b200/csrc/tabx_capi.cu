@@ -17,6 +17,7 @@ namespace tabx {
 cudaError_t launch_lanes(const Params& P, int W, int sm_count, cudaStream_t stream, int* grid);
 cudaError_t launch_ctrl(const Params& P, int W, int nh, int sm_count, cudaStream_t stream);
 cudaError_t launch_emit(const Params& P, int W, int sm_count, cudaStream_t stream);
+cudaError_t launch_fused_w1(const Params& P, int variant, int sm_count, cudaStream_t stream);
 cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
                             int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream);
 cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const DerivedCfg* dcfgs,
@@ -70,6 +71,11 @@ struct tabx_handle {
   int8_t* ctrl_act = nullptr;
   int cfg_version = 0, ctrl_version = -1, ctrl_nh = 0;
   int generic_shapes = 0;  // TABX_GENERIC_SHAPES=1: skip the shape-specialised kernels
+  // fused step + observation kernel (W = 1, K0 path; tabx_fused.cu): its
+  // variant, -1 = off (the default; TABX_FUSED=1 turns it on); whether the
+  // last step ran it
+  int fused = 0;
+  int fused_ran = 0;
   std::vector<tabx_config> cfg_host;  // host mirror of the table rows
   std::vector<char> cfg_host_ok;       // 0: row written on the device (tabx_levels)
   int cfg_cap = TABX_MAX_CONFIGS;
@@ -461,6 +467,10 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
     h->ctrl_act = (int8_t*)(a + o_ctl);
   const char* gen = getenv("TABX_GENERIC_SHAPES");
   h->generic_shapes = (gen && gen[0] == '1') ? 1 : 0;
+  const char* fz = getenv("TABX_FUSED");
+  const char* fzv = getenv("TABX_FUSED_VARIANT");
+  // off by default: measured 10% slower than K1 + K2
+  h->fused = (fz && fz[0] == '1') ? (fzv ? atoi(fzv) : 0) : -1;
 
   int rc = TABX_OK;
   for (int k = 0; k < n_configs; ++k) {
@@ -586,9 +596,23 @@ int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
       P.mode = MODE_STEP_K0;
     }
   }
-  TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "step launch");
-  if (ev) cudaEventRecord(ev[1], h->stream);
-  TABX_CUDA(launch_emit(P, h->W, h->sm_count, h->stream), "emit launch");
+  // fused step + observation kernel where it covers the shape; otherwise
+  // K1 then K2.  Profile slots: [refresh + K0 | fused] or [.. + K1 | K2].
+  h->fused_ran = 0;
+  if (h->W == 1 && h->fused >= 0 && P.mode == MODE_STEP_K0) {
+    if (ev) cudaEventRecord(ev[1], h->stream);
+    const cudaError_t fe = launch_fused_w1(P, h->fused, h->sm_count, h->stream);
+    if (fe == cudaSuccess) {
+      h->fused_ran = 1;
+    } else if (fe != cudaErrorNotSupported) {
+      TABX_CUDA(fe, "fused step launch");
+    }
+  }
+  if (!h->fused_ran) {
+    TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "step launch");
+    if (ev) cudaEventRecord(ev[1], h->stream);
+    TABX_CUDA(launch_emit(P, h->W, h->sm_count, h->stream), "emit launch");
+  }
   if (ev) cudaEventRecord(ev[2], h->stream);
   P.mode = MODE_RESET;
   TABX_CUDA(launch_lanes(P, h->W, h->sm_count, h->stream, nullptr), "reset launch");
@@ -856,6 +880,12 @@ int tabx_get_profile(tabx_handle* h, double* ms, int64_t* steps) {
   h->prof_pending = 0;
   for (int k = 0; k < 3; ++k) ms[k] = h->prof_ms[k];
   if (steps) *steps = h->prof_steps;
+  return TABX_OK;
+}
+
+int tabx_step_path(const tabx_handle* h, int32_t* fused) {
+  if (!h || !fused) return fail(TABX_E_ARGUMENT, "tabx_step_path: bad argument");
+  *fused = h->fused_ran;
   return TABX_OK;
 }
 

@@ -48,14 +48,14 @@ struct EmitScratch {
   uint16_t* plist;   // [N * (N - 1)], (observer << 5) | other
   float* stage;
 };
-__host__ __device__ __forceinline__ size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ __forceinline__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 template <int W>
-__host__ __device__ __forceinline__ size_t emit_view_bytes(int N) {
+__host__ __device__ __forceinline__ constexpr size_t emit_view_bytes(int N) {
   return align16((size_t)16 * N) + (size_t)4 * TABX_OWN_STRIDE * N +
          align16((size_t)4 * N * (2 * W + 1));
 }
 template <int W>
-__host__ __device__ __forceinline__ size_t emit_aux_bytes(int N, int Z, int R) {
+__host__ __device__ __forceinline__ constexpr size_t emit_aux_bytes(int N, int Z, int R) {
   return W == 1 ? align16(((size_t)N + 1 + (size_t)N * (N - 1)) * sizeof(uint16_t)) : 0;
 }
 

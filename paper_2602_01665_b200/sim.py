@@ -429,8 +429,19 @@ class BatchSim:
         with torch.cuda.device(self.device):
             nat.check(nat.lib().tabx_get_profile(self._h, ms, ct.byref(n)), "tabx_get_profile")
         k = max(n.value, 1)
-        return {"steps": n.value, "step_kernel_ms": ms[0] / k, "obs_kernel_ms": ms[1] / k,
-                "reset_kernel_ms": ms[2] / k}
+        fused = ct.c_int32()
+        nat.check(nat.lib().tabx_step_path(self._h, ct.byref(fused)), "tabx_step_path")
+        if fused.value:  # [refresh check + K0 | fused step + observation kernel | K3]
+            return {"steps": n.value, "fused": True, "ctrl_kernel_ms": ms[0] / k,
+                    "fused_kernel_ms": ms[1] / k, "reset_kernel_ms": ms[2] / k}
+        return {"steps": n.value, "fused": False, "step_kernel_ms": ms[0] / k,
+                "obs_kernel_ms": ms[1] / k, "reset_kernel_ms": ms[2] / k}
+
+    def step_path(self) -> str:
+        """'fused' when the last step ran the fused step + observation kernel."""
+        fused = ct.c_int32()
+        nat.check(nat.lib().tabx_step_path(self._h, ct.byref(fused)), "tabx_step_path")
+        return "fused" if fused.value else "split"
 
     def close(self) -> None:
         if getattr(self, "_h", None):
