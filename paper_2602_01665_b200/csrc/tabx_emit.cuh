@@ -72,11 +72,46 @@ __device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
                : "memory");
 }
 
+#ifndef TABX_EMIT_PREFETCH
+#define TABX_EMIT_PREFETCH 0  // L2 bulk prefetch one env ahead: measured 10% slower (TMA queue)
+#endif
+// (2: per-lane LSU line prefetches one env ahead)
+
+// Per-lane L2 line prefetches (LSU, no TMA, no registers held) of env b's
+// per-unit state arrays the view reads: lane = 4 * array + 128-byte piece.
+template <int W>
+__device__ __forceinline__ void prefetch_env_lines(const DevState& st, int64_t b, int N,
+                                                   int lane) {
+  const int64_t u = b * N;
+  const int a = lane >> 2, piece = lane & 3;
+  const char* base = nullptr;
+  size_t bytes = 0;
+  switch (a) {
+    case 0: base = (const char*)(st.pos + u); bytes = (size_t)16 * N; break;
+    case 1: base = (const char*)(st.hcs + u); bytes = (size_t)16 * N; break;
+    case 2: base = (const char*)(st.health + u); bytes = (size_t)8 * N; break;
+    case 3: base = (const char*)(st.cooldown + u); bytes = (size_t)8 * N; break;
+    case 4: base = (const char*)(st.ubits + u); bytes = (size_t)N; break;
+    case 5: base = (const char*)(st.vis + u * W); bytes = (size_t)4 * W * N; break;
+    case 6: base = (const char*)(st.atk + u * W); bytes = (size_t)4 * W * N; break;
+    default: break;
+  }
+  // the 128-byte lines covering [base, base + bytes): piece k = line k
+  const uintptr_t l0 = (uintptr_t)base & ~(uintptr_t)127;
+  const uintptr_t p = l0 + (uintptr_t)piece * 128;
+  if (base && p < (uintptr_t)base + bytes)
+    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
+}
+
 // Lanes 0..6 each pull one of env b's per-unit state arrays the view reads
 // into L2 (the emit loop issues this one env ahead).
 template <int W>
 __device__ __forceinline__ void prefetch_env_state(const DevState& st, int64_t b, int N,
                                                    int lane) {
+  if (TABX_EMIT_PREFETCH == 2) {
+    prefetch_env_lines<W>(st, b, N, lane);
+    return;
+  }
   const int64_t u = b * N;
   switch (lane) {
     case 0: l2_prefetch(st.pos + u, (size_t)16 * N); break;
@@ -166,9 +201,6 @@ __device__ __forceinline__ void load_view(const EmitScratch<W>& X, const DevStat
   __syncwarp();
 }
 
-#ifndef TABX_EMIT_PREFETCH
-#define TABX_EMIT_PREFETCH 0  // L2 bulk prefetch one env ahead: measured 10% slower (TMA queue)
-#endif
 
 // stage buffers per warp (2: fill one while the bulk store drains the other)
 #ifndef TABX_EMIT_NBUF

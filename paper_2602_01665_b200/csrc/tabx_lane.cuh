@@ -75,6 +75,12 @@ __device__ unsigned long long tabx_phase_cycles[16];
 #define TABX_PHASE(k) TABX_JITTER(k)
 #endif
 
+// W > 1 contact detection: 1 = pair-parallel over all the env's threads,
+// 0 = row-owned (thread a tests pairs (a, c > a))
+#ifndef TABX_PAIR_CONTACTS
+#define TABX_PAIR_CONTACTS 1
+#endif
+
 // ------------------------------------------------------------- helpers --
 constexpr uint32_t UF_ACTIVE = 1, UF_ALIVE = 2, UF_ENEMY = 4, UF_KIN = 8, UF_INJURED = 16;
 
@@ -984,7 +990,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const double tick = (U.active && running) ? dt : 0.0;
   cd = np_max(cd - tick, 0.0);
   rv = np_max(rv - tick, 0.0);
+  if (W > 1 && TABX_PAIR_CONTACTS) {  // this step's touching rows (read after the barriers below)
+#pragma unroll
+    for (int k = 0; k < W; ++k) S.touch[i * W + k] = 0u;
+  }
   env_sync<W>();
+  TABX_JITTER(200);  // (checked build) publish the new positions out of step
   S.px[i] = px;
   S.py[i] = py;
 #ifdef TABX_SELFTEST_RACE  // negative control of the checked build: W > 1 hand-off without its barrier
@@ -1030,6 +1041,64 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
       anyw |= bm;
     }
     any_touch = anyw != 0u;
+  } else if (TABX_PAIR_CONTACTS) {
+    // all 32 W threads over the N(N-1)/2 unordered pairs (a < c, row-major),
+    // each a contiguous range of ceil(NP / 32 W) pairs, so the detection is
+    // even across the env's warps (a row-owned loop gives row a N-1-a pairs:
+    // thread 0 tests 99 at N = 100, the mean is 49.5).  The observer's
+    // fields stay in registers until the range crosses into the next row; a
+    // hit sets bit c of row a in S.touch, in any order (bits commute).
+    // (S.touch rows were cleared before the position hand-off's barriers)
+    const int NP = N * (N - 1) / 2;
+    const int per = (NP + 32 * W - 1) / (32 * W);
+    const int p0 = i * per, p1 = min(p0 + per, NP);
+    if (running && p0 < p1) {
+      // row a of pair p0: the largest a with start(a) = a (2N - 1 - a) / 2 <= p0
+      const int twoN1 = 2 * N - 1;
+      const float tn = (float)twoN1;
+      int a = (int)((tn - sqrtf(fmaxf(tn * tn - 8.0f * (float)p0, 0.0f))) * 0.5f);
+      a = a < 0 ? 0 : (a > N - 2 ? N - 2 : a);
+      while (a > 0 && (a * (twoN1 - a)) / 2 > p0) --a;
+      while (a < N - 2 && ((a + 1) * (twoN1 - a - 1)) / 2 <= p0) ++a;
+      int c = p0 - (a * (twoN1 - a)) / 2 + a + 1;
+      double pxa = S.px[a], pya = S.py[a], ra = S.rad[a];
+      uint32_t ua = S.uf[a];
+      for (int p = p0; p < p1; ++p) {
+        TABX_ASSERT(a >= 0 && a < c && c < N);
+        if (ua & S.uf[c] & UF_ACTIVE) {
+          const double dx = S.px[c] - pxa, dy = S.py[c] - pya;
+          const double rs = ra + S.rad[c];
+          const float dxf = (float)dx, dyf = (float)dy;
+          const float d2f = dxf * dxf + dyf * dyf;
+          const float rs2f = (float)(rs * rs);
+          bool hit = false;
+          if (d2f < rs2f * 0.99999f && d2f > 1e-30f) {
+            hit = true;
+          } else if (!(d2f > rs2f * 1.00001f)) {
+            const double dist = slow_sqrt(dx * dx + dy * dy);
+            hit = (dist == 0.0 ? rs : rs - dist) > 0.0;
+          }
+          if (hit) atomicOr(&S.touch[a * W + (c >> 5)], 1u << (c & 31));
+        }
+        if (++c == N) {  // next row
+          ++a;
+          c = a + 1;
+          if (a < N - 1) {
+            pxa = S.px[a];
+            pya = S.py[a];
+            ra = S.rad[a];
+            ua = S.uf[a];
+          }
+        }
+      }
+    }
+    env_sync<W>();
+    bool mine = false;
+#pragma unroll
+    for (int k = 0; k < W; ++k) mine |= S.touch[i * W + k] != 0u;
+    env_ballot<W>(mine, S, i, rowm);
+#pragma unroll
+    for (int k = 0; k < W; ++k) any_touch |= rowm[k] != 0u;
   } else {
     uint32_t trow[W];
 #pragma unroll
@@ -1070,6 +1139,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 #pragma unroll
     for (int k = 0; k < W; ++k) any_touch |= rowm[k] != 0u;
   }
+  TABX_PHASE(10);  // (K0 mode: slot 10 = integrate + contact detection)
   double vfx = vux, vfy = vuy;
   if (any_touch) {
     S.vx[i] = vux;
@@ -1334,11 +1404,19 @@ __host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
 #ifndef TABX_MIN_BLOCKS
 #define TABX_MIN_BLOCKS 4
 #endif
+// W > 1 (one env per CTA of 32 W threads): resident warps per SM the
+// register budget is cut for (C4 step kernels: unconstrained 254 registers
+// at 8 warps/SM 11.2 ms; 16 warps at 128 registers 7.8 ms; 24 warps at 80
+// registers 7.3 ms)
+#ifndef TABX_WN_WARPS
+#define TABX_WN_WARPS 24
+#endif
+#define TABX_MIN_BLOCKS_WN(W) (TABX_WN_WARPS / (W) > 1 ? TABX_WN_WARPS / (W) : 1)
 // K1 (MODE_STEP / MODE_INIT / MODE_REFRESH) and K3 (MODE_RESET).
 // One kernel per mode (M): the step kernel carries no reset / emitter code,
 // which keeps its instruction footprint and register allocation to its own.
 template <int W, int EPB, int M, int NF = 0, int ZF = 0>
-__global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : 1))
+__global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : TABX_MIN_BLOCKS_WN(W)))
     lane_kernel(const Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EnvSmem<W>* envs = reinterpret_cast<EnvSmem<W>*>(smem_raw);

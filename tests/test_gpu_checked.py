@@ -39,12 +39,14 @@ if not torch.cuda.is_available():  # pragma: no cover
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CHECKED = os.path.join(ROOT, "paper_2602_01665_b200", "_tabx_checked.so")
+SELFTEST = os.path.join(ROOT, "paper_2602_01665_b200", "_tabx_selftest_race.so")
 
 SELECT = ("test_golden_case_parity or test_injected_state_single_step or "
           "test_many_zones_match_oracle or test_two_word_rows_with_zones_match_oracle or "
           "test_mixed_configs_and_reset_env_swap or test_controller_pass_mixed_heuristic_counts "
           "or test_action_mask_error or test_dead_units or test_fov_boundary or "
-          "test_slot_recycling or test_batch_of_levels_and_respawn")
+          "test_slot_recycling or test_batch_of_levels_and_respawn or "
+          "test_fused_small_and_ragged_batches_match_oracle")
 
 
 def test_parity_cases_through_checked_kernels():
@@ -53,7 +55,8 @@ def test_parity_cases_through_checked_kernels():
     env = dict(os.environ, TABX_LIB=CHECKED)
     cmd = [sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
            os.path.join(HERE, "test_gpu_parity.py"), os.path.join(HERE, "test_gpu_reconfig.py"),
-           os.path.join(HERE, "test_gpu_levels.py"), "-k", SELECT]
+           os.path.join(HERE, "test_gpu_levels.py"), os.path.join(HERE, "test_gpu_fused.py"),
+           "-k", SELECT]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=3000)
     tail = (r.stdout + r.stderr)[-4000:]
     print(r.stdout[-600:])
@@ -62,3 +65,20 @@ def test_parity_cases_through_checked_kernels():
     import re
     m = re.search(r"(\d+) passed", r.stdout)
     assert m and int(m.group(1)) >= 30, tail  # the selection really ran
+
+
+def test_checked_build_catches_a_dropped_barrier():
+    """Negative control: the checked build with ONE barrier removed (the
+    W > 1 step kernel's hand-off between publishing the integrated positions
+    and the contact pass, -DTABX_SELFTEST_RACE) must fail the W > 1 parity
+    cases -- evidence that the lane jitter exposes a missing barrier."""
+    if not os.path.exists(SELFTEST):
+        pytest.fail(f"{SELFTEST} missing: run build() (it builds the negative control too)")
+    env = dict(os.environ, TABX_LIB=SELFTEST)
+    sel = ("test_golden_case_parity and (c4 or w8) or test_injected_state_single_step or "
+           "test_two_word_rows_with_zones_match_oracle")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+           os.path.join(HERE, "test_gpu_parity.py"), "-k", sel]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=3000)
+    print(r.stdout[-800:])
+    assert r.returncode != 0 and " failed" in r.stdout, (r.stdout + r.stderr)[-3000:]

@@ -23,10 +23,10 @@ from paper_2602_01665_b200.rng import lane_seeds  # noqa: E402
 from paper_2602_01665_b200.scenario import builtin_scenario  # noqa: E402
 from paper_2602_01665_b200.sim import BatchSim  # noqa: E402
 
-PHASES = ["state load + masks", "action mask + controllers", "integrate + contacts",
+PHASES = ["state load + masks", "action mask + controllers", "contact solve (Gauss-Seidel)",
           "boundary + rotation", "stage-8 caches", "combat, reveal, lava, deaths",
           "team ratios, rewards, termination", "outputs + stats", "state write-back",
-          "  (in controllers) mask + swamp", "  (in controllers) vis/atk cache loads",
+          "  (in controllers) mask + swamp", "  integrate + contact detection (+ MODE_STEP vis/atk loads)",
           "  (in controllers) scripted_action", "  (in caches) zone_bits",
           "  (in caches) publish + build_masks",
           "    (in scripted, lowest heuristic lane) statics + target loop",
