@@ -51,6 +51,20 @@ __device__ __forceinline__ void tabx_poison(void* p, size_t bytes, int t, int n)
   } while (0)
 #endif
 
+// ---- path counters (-DTABX_COUNT_PROF, tools/count_prof.py): how often the
+// exact float64 fallbacks run; slot k of tabx_phase_cycles (the phase-profile
+// array, read back with tabx_debug_phase_cycles)
+#if defined(TABX_PHASE_PROF) || defined(TABX_COUNT_PROF)
+__device__ unsigned long long tabx_phase_cycles[16];
+#endif
+#ifdef TABX_COUNT_PROF
+#define TABX_COUNT(k) atomicAdd(&::tabx::tabx_phase_cycles[k], 1ull)
+#else
+#define TABX_COUNT(k) \
+  do {                \
+  } while (0)
+#endif
+
 constexpr int A_ROTATE = 4;
 constexpr int A_ATTACK = 5;
 constexpr int A_NOOP = 6;
@@ -157,6 +171,7 @@ struct Params {
 };
 
 __device__ __noinline__ static bool zone_exact(double ex, double ey, double ax, double ay) {
+  TABX_COUNT(6);
   const double qx = ex / ax;
   const double qy = ey / ay;
   return qx * qx + qy * qy <= 1.0;
@@ -206,7 +221,10 @@ __device__ __forceinline__ float f32_quot(double x, double y, double ry) {
   // and not zero
   const uint32_t e = (hi >> 20) & 0x7FFu;
   const bool odd = (e - 898u) > 247u && ((hi & 0x7FFFFFFFu) | lo) != 0u;
-  if (mid || odd) q = slow_div(x, y);
+  if (mid || odd) {
+    TABX_COUNT(7);
+    q = slow_div(x, y);
+  }
   return __double2float_rn(q);
 }
 

@@ -49,8 +49,7 @@ __device__ __forceinline__ double uniform53(uint64_t seed, uint64_t step, uint64
 // Built only with -DTABX_PHASE_PROF (tools): lane 0 of each env accumulates
 // SM clock cycles per step phase into tabx_phase_cycles (read back with
 // tabx_debug_phase_cycles).  The default build compiles the marks to nothing.
-#ifdef TABX_PHASE_PROF
-__device__ unsigned long long tabx_phase_cycles[16];
+#if defined(TABX_PHASE_PROF) && !defined(TABX_COUNT_PROF)
 #define TABX_PHASE_BEGIN() long long ph_t0_ = clock64()
 #define TABX_PHASE(k)                                                  \
   do {                                                                 \
@@ -298,6 +297,7 @@ __device__ __forceinline__ float rsqrt_approx(float x) {
 __device__ __forceinline__ bool closer(double a2, double b2) {
   if (!(a2 < b2)) return false;
   if (a2 < b2 * (1.0 - 1e-14)) return true;
+  TABX_COUNT(8);
   return slow_sqrt(a2) < slow_sqrt(b2);
 }
 
@@ -349,6 +349,7 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
   int tgt = -1;
   const uint32_t uf_i = S.uf[i];
   if (uf_i & UF_ACTIVE) {  // vis requires both active; atk requires vis
+    TABX_COUNT(9);
     const double px = S.px[i], py = S.py[i], ch = S.ch[i], sh = S.sh[i];
     const float chf = (float)ch, shf = (float)sh;
     const float sr2 = (float)(srange * srange);
@@ -381,6 +382,7 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
       while (m) {
         const int j = (k << 5) + __ffs(m) - 1;
         m &= m - 1;
+        TABX_COUNT(0);
         const Seen e = exact_seen(S.px[j] - px, S.py[j] - py, ch, sh, srange, cos_half);
         if (e.seen) seen[k] |= 1u << (j & 31);
       }
@@ -409,7 +411,7 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
     }
     vis[i >> 5] |= 1u << (i & 31);  // distance 0, cos_dev 1: sees itself
     const float reachf = (float)reach, radf = (float)rad;
-    double best = 0.0;
+    double best = 0.0;  // squared distance of the target so far
 #pragma unroll
     for (int k = 0; k < W; ++k) {
       uint32_t m = cand[k];
@@ -434,13 +436,18 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
         } else if (gapf > rj2f + mb) {
           box = false;
         } else {
+          TABX_COUNT(1);
           box = exact_box(dx, dy, ch, sh, reach, rad, rj);
         }
         if (!box) continue;
         atk[k] |= 1u << (j & 31);
-        const double dist = sqrt(dx * dx + dy * dy);
-        if (tgt < 0 || dist < best) {
-          best = dist;
+        TABX_COUNT(5);
+        // nearest attackable, first index on ties of the rounded distances
+        // (combat.py argmin over sqrt(dx^2 + dy^2)): squares compared, the
+        // roots only for near-ties (closer)
+        const double d2 = dx * dx + dy * dy;
+        if (tgt < 0 || closer(d2, best)) {
+          best = d2;
           tgt = j;
         }
       }
@@ -1031,6 +1038,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
           if (d2f < rs2f * 0.99999f && d2f > 1e-30f) {
             hit = true;
           } else if (!(d2f > rs2f * 1.00001f)) {
+            TABX_COUNT(2);
             const double dist = slow_sqrt(dx * dx + dy * dy);
             hit = (dist == 0.0 ? rs : rs - dist) > 0.0;
           }
@@ -1075,6 +1083,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
           if (d2f < rs2f * 0.99999f && d2f > 1e-30f) {
             hit = true;
           } else if (!(d2f > rs2f * 1.00001f)) {
+            TABX_COUNT(3);
             const double dist = slow_sqrt(dx * dx + dy * dy);
             hit = (dist == 0.0 ? rs : rs - dist) > 0.0;
           }
@@ -1126,6 +1135,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
           m &= m - 1;
           const double dx = S.px[j] - px, dy = S.py[j] - py;
           const double rs = U.rad + S.rad[j];
+          TABX_COUNT(4);
           const double dist = slow_sqrt(dx * dx + dy * dy);
           const double depth = dist == 0.0 ? rs : rs - dist;
           if (depth > 0.0) trow[k] |= 1u << (j & 31);

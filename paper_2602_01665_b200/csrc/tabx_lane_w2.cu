@@ -13,7 +13,7 @@ cudaError_t launch_emit_w2(const Params& P, int sm_count, cudaStream_t stream) {
 }
 // Phase cycle counters of the instrumented build (zeros otherwise).
 cudaError_t phase_cycles_w2(unsigned long long* host16, int reset) {
-#ifdef TABX_PHASE_PROF
+#if defined(TABX_PHASE_PROF) || defined(TABX_COUNT_PROF)
   cudaError_t e = cudaMemcpyFromSymbol(host16, tabx_phase_cycles, 16 * sizeof(unsigned long long));
   if (e == cudaSuccess && reset) {
     static const unsigned long long zero[16] = {};
