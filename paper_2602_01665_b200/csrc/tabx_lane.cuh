@@ -1003,6 +1003,11 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   }
   env_sync<W>();
   TABX_JITTER(200);  // (checked build) publish the new positions out of step
+#ifdef TABX_SELFTEST_RACE
+  // negative control: half the threads publish 20 us late, past the
+  // contact filter's and the exact fallback's reads of the positions
+  if ((threadIdx.x * 0x9E3779B9u) >> 31) __nanosleep(20000);
+#endif
   S.px[i] = px;
   S.py[i] = py;
 #ifdef TABX_SELFTEST_RACE  // negative control of the checked build: W > 1 hand-off without its barrier
