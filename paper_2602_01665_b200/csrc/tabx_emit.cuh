@@ -73,7 +73,7 @@ __device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
 }
 
 #ifndef TABX_EMIT_PREFETCH
-#define TABX_EMIT_PREFETCH 0  // L2 bulk prefetch one env ahead: measured 10% slower (TMA queue)
+#define TABX_EMIT_PREFETCH 0  // 1: TMA L2 prefetch one env ahead (10% slower), 2: LSU line prefetch one env ahead (2% slower), 3: LSU prefetch two chunks ahead (4% slower)
 #endif
 // (2: per-lane LSU line prefetches one env ahead)
 
@@ -211,10 +211,28 @@ __device__ __forceinline__ void load_view(const EmitScratch<W>& X, const DevStat
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// L2 policy of the row stream's bulk stores.  Evict-first (the rows are
+// never read back on the device path) measured faster for the one-warp-per-
+// env emitter (W = 1: C3 262,144 envs K2 1.665 -> 1.611 ms, C3 65,536
+// -2%, C2 262,144 -1%, C2 65,536 +0.7%) and slower for W = 4 (C4 15.5 ->
+// 15.9 ms), so it is used for W = 1 only; TABX_EMIT_EVICT_FIRST=0 turns it off.
+#ifndef TABX_EMIT_EVICT_FIRST
+#define TABX_EMIT_EVICT_FIRST 1
+#endif
+template <bool EF>
 __device__ __forceinline__ void bulk_s2g(void* g, const void* s, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g),
-               "r"(smem_addr(s)), "r"(bytes)
-               : "memory");
+  if constexpr (EF && TABX_EMIT_EVICT_FIRST) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    asm volatile(
+        "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::"l"(g),
+        "r"(smem_addr(s)), "r"(bytes), "l"(pol)
+        : "memory");
+  } else {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g),
+                 "r"(smem_addr(s)), "r"(bytes)
+                 : "memory");
+  }
 }
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
@@ -233,6 +251,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 // dst[gs, gs+count) <- stage[pad, pad+count), pad = gs & 3: the 16-byte
 // aligned interior by one TMA bulk store (lane 0), the <= 3-float head and
 // tail by plain stores.
+template <bool EF>
 __device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs, int count,
                                             const float* stage, int lane) {
   const int pad = (int)(gs & 3);
@@ -240,7 +259,7 @@ __device__ __forceinline__ void flush_stage(float* __restrict__ dst, int64_t gs,
   const int64_t a1 = (gs + count) & ~(int64_t)3;
   TABX_ASSERT(gs >= 0 && count > 0 && ((uintptr_t)(dst + a0) & 15u) == 0);
   if (a1 > a0) {
-    if (lane == 0) bulk_s2g(dst + a0, stage + pad + (a0 - gs), (uint32_t)((a1 - a0) * 4));
+    if (lane == 0) bulk_s2g<EF>(dst + a0, stage + pad + (a0 - gs), (uint32_t)((a1 - a0) * 4));
     // <= 3 head floats on lanes 0..2, <= 3 tail floats on lanes 4..6
     const int head = (int)(a0 - gs), t0 = (int)(a1 - gs);
     const int e = lane < 4 ? lane : t0 + lane - 4;
@@ -288,7 +307,8 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
                           float* __restrict__ glob, int64_t b, int N, int Z, int D, int G, int R,
                           int SF, const tabx_config* __restrict__ C,
                           const DerivedCfg* __restrict__ DC, int lane, int& buf, bool drain,
-                          __nv_bfloat16* __restrict__ o16 = nullptr, int ld16 = 0) {
+                          __nv_bfloat16* __restrict__ o16 = nullptr, int ld16 = 0,
+                          const DevState* pf_st = nullptr, int64_t pf_b = -1) {
   const EmitEnv<W>& E = X.E;
   const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
   const int M = N - 1;
@@ -320,6 +340,11 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
     for (int r0 = 0; r0 < N; r0 += R) {
       const int nr = min(R, N - r0);
       const int64_t gs = (b * N + r0) * (int64_t)D;
+#if TABX_EMIT_PREFETCH == 3
+      // the next env's view lines into L2 two chunks before this env ends
+      // (a longer distance loses them to the row stream's L2 turnover)
+      if (pf_b >= 0 && r0 + 2 * R >= N && r0 + R < N) prefetch_env_lines<W>(*pf_st, pf_b, N, lane);
+#endif
       TABX_ASSERT(nr > 0 && (pad_fits(gs, nr * D, SF)));
       TABX_JITTER(301);
       float* st = X.stage + buf * SF;
@@ -432,7 +457,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
       TABX_JITTER(302);
       fence_proxy_async();
       __syncwarp();
-      if (obs) flush_stage(obs, gs, nr * D, st, lane);
+      if (obs) flush_stage<W == 1>(obs, gs, nr * D, st, lane);
       if (F16 && o16) {
         // 8 bfloat16 (16 bytes) per store, zero past obs_dim; the stage is
         // only read, beside the bulk store reading it.  Rows start 8-byte
@@ -478,7 +503,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
     TABX_JITTER(303);
     fence_proxy_async();
     __syncwarp();
-    flush_stage(glob, gs, G, st, lane);
+    flush_stage<W == 1>(glob, gs, G, st, lane);
     buf = TABX_EMIT_NBUF == 1 ? 0 : buf ^ 1;
   }
   if (drain) {
@@ -621,7 +646,7 @@ __global__ void __launch_bounds__(32 * EPW,
   // does not start with a dependent chain of DRAM round trips
   int32_t k_next = b < P.B ? st.cfg[b] : 0;
   uint8_t f_next = b < P.B ? st.flags[b] : 0;
-#if TABX_EMIT_PREFETCH
+#if TABX_EMIT_PREFETCH && TABX_EMIT_PREFETCH != 3
   if (b < P.B) prefetch_env_state<W>(st, b, N, lane);
 #endif
   for (; b < P.B; b += stride) {
@@ -630,7 +655,7 @@ __global__ void __launch_bounds__(32 * EPW,
     if (b + stride < P.B) {
       k_next = st.cfg[b + stride];
       f_next = st.flags[b + stride];
-#if TABX_EMIT_PREFETCH
+#if TABX_EMIT_PREFETCH && TABX_EMIT_PREFETCH != 3
       prefetch_env_state<W>(st, b + stride, N, lane);
 #endif
     }
@@ -643,7 +668,7 @@ __global__ void __launch_bounds__(32 * EPW,
     if (!ob && !gb && !o16) continue;
     load_view<W>(X, st, b, N, Z, C, DC, lane);
     emit_lane<W, F16>(X, ob, gb, b, N, Z, D, G, R, SF, C, DC, lane, buf, false, o16,
-                      (int)P.out.observations_bf16_ld);
+                      (int)P.out.observations_bf16_ld, &st, b + stride < P.B ? b + stride : -1);
   }
   if (lane == 0) bulk_wait_all();
 }

@@ -19,7 +19,17 @@ import io
 import json
 import sys
 
-PEAK_GBS = 6451.2
+def _peak() -> float:
+    import os
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6547.5
+
+
+PEAK_GBS = _peak()
 
 
 def main(argv) -> int:
