@@ -7,6 +7,14 @@
 //   differ by up to 2 ulp.  To reproduce the reference bit for bit the
 //   device runs a restatement of glibc 2.39's algorithm, including the
 //   exact fused multiply-adds of its x86-64 FMA build.
+//   Provenance / attribution: the range reduction constants, the
+//   polynomial coefficients and the branch structure of __sin / __cos follow
+//   the GNU C Library's sysdeps/ieee754/dbl-64/s_sin.c and usncs.h (glibc
+//   2.39, Copyright (C) 2001-2024 Free Software Foundation, Inc., licensed
+//   under the GNU Lesser General Public License v2.1 or later; originally
+//   contributed by IBM).  The table sincos_table.inc is regenerated from its
+//   definition (sin/cos of i/128 in 70-digit arithmetic,
+//   tools/gen_sincos_table.py), not copied.
 // * np_max/np_min/np_clip/np_remainder: numpy's ufunc definitions.
 // * pairwise_sum: numpy's pairwise add.reduce (8 accumulators, blocks of
 //   128, recursive split), used for the team health ratio sums
