@@ -283,7 +283,8 @@ def measure_device(cx: Ctx, key: str, per: int, steps: int, warmup: int, seed: i
            "agent_steps_per_s": total * steps / (elapsed_ms / 1000.0) * len(sc.units),
            "envs": total, "envs_per_gpu": per, "n_units": N, "n_zones": Z,
            "clocks": clk.summary(), "step_path": sim.step_path(),
-           "gpu_launches": (launches_per_step(per) - (sim.step_path() == "fused")) * steps}
+           "gpu_launches": {"split": launches_per_step(per), "fused": launches_per_step(per) - 1,
+                            "single": 1}[sim.step_path()] * steps}
     if profile:
         # per-kernel times (roofline) from a second pass of the same length with
         # CUDA events around every kernel, so their host cost stays out of `value`
@@ -319,7 +320,10 @@ def roofline(key: str, N: int, Z: int, per: int, kern_ms: float, kprof: dict) ->
     obs_bytes = 4 * N * D + 4 * G + 57 * N + 5  # writes + the per-unit view it reads
     step_bytes = bytes_per - (4 * N * D + 4 * G)
     kernels = []
-    if kprof.get("fused"):
+    if kprof.get("fused") == "single":
+        rows = (("single_kernel (K1 + K2 + K3 of a small batch in one launch: step, observation "
+                 "rows, auto-resets)", kprof["single_kernel_ms"], step_bytes + obs_bytes),)
+    elif kprof.get("fused"):
         # refresh check + K0 (re-reads of the unit view only), then one fused
         # kernel: the step's state traffic + the observation stream
         rows = (("ctrl_kernels (refresh check + K0 heuristic-controller pass)",
@@ -339,7 +343,7 @@ def roofline(key: str, N: int, Z: int, per: int, kern_ms: float, kprof: dict) ->
         if nbytes and ms > 0:
             gbs = nbytes * per / (ms / 1000.0) / 1e9
             ent.update({"bytes_per_env_step": nbytes, "achieved_gbs": gbs, "frac": gbs / peak})
-        if ("obs_kernel" in name or "fused_kernel" in name) and ms > 0:
+        if ("obs_kernel" in name or "fused_kernel" in name or "single_kernel" in name) and ms > 0:
             strict = (4 * N * D + 4 * G) * per / (ms / 1000.0) / 1e9
             ent["frac_obs_bytes_only"] = strict / peak
         kernels.append(ent)
@@ -582,7 +586,7 @@ def run_gpu_arm(args) -> int:
                                        "prices copying them out)"},
             "roofline": head["roofline"],
             "e2e": e2e,
-            "gpu_launches": head["gpu_launches"],
+            "gpu_launches": head["gpu_launches"], "step_path": head.get("step_path"),
             "clocks": head["clocks"],
             "episode_stats": head["episode_stats"],
         }

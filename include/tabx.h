@@ -323,11 +323,15 @@ int tabx_set_profiling(tabx_handle* h, int32_t enable);
 int tabx_get_profile(tabx_handle* h, double* ms, int64_t* steps);
 
 /*
- * Which kernels the last tabx_step ran: *fused = 1 when the fused step +
- * observation kernel did (W = 1, heuristic-controller pass on, a shape with
- * specialised kernels, and TABX_FUSED=1 at creation: it is off by default), 0 for the separate step
- * and observation kernels.  With fused = 1 the profile's ms[0] covers the
- * refresh check + controller pass and ms[1] the fused kernel.
+ * Which kernels the last tabx_step ran: *fused = 0 for the separate step,
+ * observation and reset kernels; 1 when the fused step + observation kernel
+ * did (W = 1, heuristic-controller pass on, a shape with specialised kernels,
+ * and TABX_FUSED=1 at creation: it is off by default); 2 for the
+ * single-launch step (W = 1 batches below TABX_SINGLE_MAX_ENVS = 4,096 lanes
+ * stepped with the in-kernel controller: step, observation rows and
+ * auto-resets in one kernel).  With fused = 1 the profile's ms[0] covers the
+ * refresh check + controller pass and ms[1] the fused kernel; with 2, ms[1]
+ * is the single kernel.
  */
 int tabx_step_path(const tabx_handle* h, int32_t* fused);
 

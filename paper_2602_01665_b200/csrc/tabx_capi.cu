@@ -18,6 +18,7 @@ cudaError_t launch_lanes(const Params& P, int W, int sm_count, cudaStream_t stre
 cudaError_t launch_ctrl(const Params& P, int W, int nh, int sm_count, cudaStream_t stream);
 cudaError_t launch_emit(const Params& P, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_fused_w1(const Params& P, int variant, int sm_count, cudaStream_t stream);
+cudaError_t launch_small_w1(const Params& P, int sm_count, cudaStream_t stream);
 cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
                             int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream);
 cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const DerivedCfg* dcfgs,
@@ -75,7 +76,11 @@ struct tabx_handle {
   // variant, -1 = off (the default; TABX_FUSED=1 turns it on); whether the
   // last step ran it
   int fused = 0;
-  int fused_ran = 0;
+  int fused_ran = 0;  // 1: fused step + observation kernel, 2: single-launch small step
+  // single-launch step (K1 + K2 + K3 in one kernel) for W = 1 batches below
+  // this many lanes stepped with the in-kernel controller (TABX_SINGLE_MAX_ENVS,
+  // 0 = off)
+  int64_t single_max = 4096;
   std::vector<tabx_config> cfg_host;  // host mirror of the table rows
   std::vector<char> cfg_host_ok;       // 0: row written on the device (tabx_levels)
   int cfg_cap = TABX_MAX_CONFIGS;
@@ -471,6 +476,8 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   const char* fzv = getenv("TABX_FUSED_VARIANT");
   // off by default: measured 10% slower than K1 + K2
   h->fused = (fz && fz[0] == '1') ? (fzv ? atoi(fzv) : 0) : -1;
+  const char* smx = getenv("TABX_SINGLE_MAX_ENVS");
+  if (smx) h->single_max = atoll(smx);
 
   int rc = TABX_OK;
   for (int k = 0; k < n_configs; ++k) {
@@ -599,6 +606,20 @@ int tabx_step(tabx_handle* h, const int64_t* actions, const tabx_outputs* out) {
   // fused step + observation kernel where it covers the shape; otherwise
   // K1 then K2.  Profile slots: [refresh + K0 | fused] or [.. + K1 | K2].
   h->fused_ran = 0;
+  if (h->W == 1 && P.mode == MODE_STEP && h->B < h->single_max) {
+    // the whole step in one launch (small batches are launch-latency bound)
+    if (ev) cudaEventRecord(ev[1], h->stream);
+    const cudaError_t se = launch_small_w1(P, h->sm_count, h->stream);
+    if (se == cudaSuccess) {
+      if (ev) {
+        cudaEventRecord(ev[2], h->stream);
+        cudaEventRecord(ev[3], h->stream);
+      }
+      h->fused_ran = 2;
+      return TABX_OK;
+    }
+    if (se != cudaErrorNotSupported) TABX_CUDA(se, "single-launch step");
+  }
   if (h->W == 1 && h->fused >= 0 && P.mode == MODE_STEP_K0) {
     if (ev) cudaEventRecord(ev[1], h->stream);
     const cudaError_t fe = launch_fused_w1(P, h->fused, h->sm_count, h->stream);

@@ -274,3 +274,112 @@ cudaError_t launch_fused_w1(const Params& P, int variant, int sm_count, cudaStre
 }
 
 }  // namespace tabx
+
+// ------------------------------------------------- single-launch small step --
+// Small batches (below the controller-pass threshold, W = 1): the step is
+// launch-latency bound (C1, 256 envs: K1 + K2 + K3 back to back, ~30 us for
+// three dependent launches), so the whole step runs as ONE launch: each warp
+// steps its environment with the in-kernel controller (run_lane MODE_STEP),
+// streams its observation rows (terminal rows to final_* when the lane's
+// auto-reset is pending), and then performs that reset itself (run_lane
+// MODE_RESET: respawn, fresh caches, fresh observation).  The last CTA to
+// finish advances the device step counter, as K3 does.  The batch-coupled
+// cache refresh stays deferred to the next step's start (same ring), so the
+// per-environment code and the bits are those of K1 + K2 + K3.
+namespace tabx {
+
+template <int NF, int ZF, int EPB>
+__global__ void __launch_bounds__(32 * EPB, TABX_MIN_BLOCKS) step_small_kernel(const Params P) {
+  constexpr size_t env_bytes = (sizeof(EnvSmem<1>) * EPB + 15) & ~(size_t)15;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (P.sync->err_index != NO_ERROR) return;  // an action violated the mask: no mutation
+  const int N = NF ? NF : P.N, Z = ZF ? ZF : P.Z;
+  EnvSmem<1>* envs = reinterpret_cast<EnvSmem<1>*>(smem_raw);
+  const size_t view_bytes = reset_view_bytes<1>(P);
+  const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned char* scratch = smem_raw + env_bytes + g * view_bytes;
+  const uint32_t step_no = P.sync->step;
+  const bool refresh = P.sync->refresh[step_no % 3] != 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.sync->refresh[(step_no + 2) % 3] = 0;
+  {  // pair table (N <= 32)
+    int p = 0;
+    for (int a = 0; a < N; ++a) {
+      const int cnt = N - 1 - a;
+      for (int q = lane; q < cnt; q += 32) envs[g].ptab[p + q] = (uint16_t)((a << 8) | (a + 1 + q));
+      p += cnt;
+    }
+    __syncwarp();
+  }
+  const int R = emit_rows(N, P.D, TABX_EMIT_BUDGET);
+  const int SF = emit_stage_floats(N, P.D, P.G, R);
+  const DevState& st = P.st;
+  for (int64_t b = (int64_t)blockIdx.x * EPB + g; b < P.B; b += (int64_t)gridDim.x * EPB) {
+    TABX_POISON(&envs[g], offsetof(EnvSmem<1>, ptab), lane, 32);
+    __syncwarp();
+    run_lane<1, MODE_STEP, NF, ZF>(P, b, lane, envs[g], nullptr, refresh, step_no);
+    __syncwarp();  // the warp's own state stores, read back below
+    const int32_t kc = st.cfg[b];
+    const tabx_config* C = P.cfgs + kc;
+    const DerivedCfg* DC = P.dcfgs + kc;
+    const bool pending = (st.flags[b] & F_PEND) != 0;
+    float* ob = pending ? P.out.final_observations : P.out.observations;
+    float* gb = pending ? P.out.final_global_state : P.out.global_state;
+    __nv_bfloat16* o16 = pending ? nullptr : (__nv_bfloat16*)P.out.observations_bf16;
+    if (ob || gb || o16) {
+      const EmitScratch<1> X = emit_scratch<1>(scratch, N, Z, R);
+      int buf = 0;
+      load_view<1>(X, st, b, N, Z, C, DC, lane);
+      if (o16)
+        emit_lane<1, true>(X, ob, gb, b, N, Z, P.D, P.G, R, SF, C, DC, lane, buf, true, o16,
+                           (int)P.out.observations_bf16_ld);
+      else
+        emit_lane<1>(X, ob, gb, b, N, Z, P.D, P.G, R, SF, C, DC, lane, buf, true);
+    }
+    if (pending) {
+      // K3 for this lane (its stage buffers were drained above)
+      TABX_POISON(&envs[g], offsetof(EnvSmem<1>, ptab), lane, 32);
+      __syncwarp();
+      run_lane<1, MODE_RESET, NF, ZF>(P, b, lane, envs[g], scratch, refresh, step_no);
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+  // the step ends here: the last CTA advances the device step counter
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t ticket = atomicAdd(&P.sync->blocks_done, 1u);
+    if (ticket == gridDim.x - 1) {
+      P.sync->blocks_done = 0;
+      P.sync->any_pend = 0;
+      P.sync->step = step_no + 1;
+      __threadfence();
+    }
+  }
+}
+
+template <int NF, int ZF>
+cudaError_t launch_small_shape(const Params& P, int sm_count, cudaStream_t stream) {
+  constexpr int EPB = 4;
+  const size_t env_bytes = (sizeof(EnvSmem<1>) * EPB + 15) & ~(size_t)15;
+  const size_t smem = env_bytes + reset_view_bytes<1>(P) * EPB;
+  int per_sm = 0;
+  auto kern = step_small_kernel<NF, ZF, EPB>;
+  cudaError_t e = launch_geometry((const void*)kern, 32 * EPB, smem, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorNotSupported;
+  const int64_t need = (P.B + EPB - 1) / EPB, cap = (int64_t)sm_count * per_sm;
+  int grid = (int)(need < cap ? need : cap);
+  if (grid < 1) grid = 1;
+  kern<<<grid, 32 * EPB, smem, stream>>>(P);
+  return cudaGetLastError();
+}
+
+// The single-launch step for W = 1 batches stepped with the in-kernel
+// controller (MODE_STEP); cudaErrorNotSupported otherwise.
+cudaError_t launch_small_w1(const Params& P, int sm_count, cudaStream_t stream) {
+  if (P.mode != MODE_STEP) return cudaErrorNotSupported;
+  if (!P.generic_shapes && P.N == 6 && P.Z == 0) return launch_small_shape<6, 0>(P, sm_count, stream);
+  return launch_small_shape<0, 0>(P, sm_count, stream);
+}
+
+}  // namespace tabx

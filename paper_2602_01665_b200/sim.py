@@ -431,6 +431,8 @@ class BatchSim:
         k = max(n.value, 1)
         fused = ct.c_int32()
         nat.check(nat.lib().tabx_step_path(self._h, ct.byref(fused)), "tabx_step_path")
+        if fused.value == 2:  # the single-launch step (small batches)
+            return {"steps": n.value, "fused": "single", "single_kernel_ms": ms[1] / k}
         if fused.value:  # [refresh check + K0 | fused step + observation kernel | K3]
             return {"steps": n.value, "fused": True, "ctrl_kernel_ms": ms[0] / k,
                     "fused_kernel_ms": ms[1] / k, "reset_kernel_ms": ms[2] / k}
@@ -438,10 +440,12 @@ class BatchSim:
                 "obs_kernel_ms": ms[1] / k, "reset_kernel_ms": ms[2] / k}
 
     def step_path(self) -> str:
-        """'fused' when the last step ran the fused step + observation kernel."""
+        """Kernels of the last step: 'split' (K1, K2, K3 and, from 4,096 lanes,
+        the controller pass), 'fused' (fused step + observation kernel, opt-in)
+        or 'single' (the whole step in one launch, small batches)."""
         fused = ct.c_int32()
         nat.check(nat.lib().tabx_step_path(self._h, ct.byref(fused)), "tabx_step_path")
-        return "fused" if fused.value else "split"
+        return {0: "split", 1: "fused", 2: "single"}[fused.value]
 
     def close(self) -> None:
         if getattr(self, "_h", None):

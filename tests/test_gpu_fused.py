@@ -99,3 +99,57 @@ def test_fused_small_and_ragged_batches_match_oracle(B, monkeypatch):
             bad += compare_state(gpu.export_state(), ora.sim, f"fused B={B} t={t}")
         assert not bad, "\n".join(bad[:10])
     gpu.close()
+
+
+def _pair_single(sc, B, seeds, monkeypatch, **kw):
+    """(single-launch step, split K1 + K2 + K3), both with the in-kernel
+    controller (TABX_NO_K0=1)."""
+    monkeypatch.setenv("TABX_NO_K0", "1")
+    sims = []
+    for mx in ("4096", "0"):
+        monkeypatch.setenv("TABX_SINGLE_MAX_ENVS", mx)
+        sims.append(BatchSim([sc] * B, seeds, auto_reset=True, device="cuda:0", **kw))
+    return sims
+
+
+@pytest.mark.parametrize("scen,B,steps", [("c1_3v3", 256, 410), ("c3_10v10_terrain", 600, 40),
+                                          ("c2_10v10", 37, 30)])
+def test_single_launch_step_equals_split(scen, B, steps, monkeypatch):
+    """The single-launch step (small batches: step, observation rows and the
+    auto-resets in one kernel) against K1 + K2 + K3: every output and the
+    state, across auto-resets (C1 over 410 steps crosses the lockstep
+    truncation at t = 400)."""
+    sc = builtin_scenario(scen).scripted()
+    single, split = _pair_single(sc, B, np.arange(B, dtype=np.uint64) * 7 + 3, monkeypatch)
+    resets = 0
+    for t in range(steps):
+        outs = (single.step(None), split.step(None))
+        assert single.step_path() == "single" and split.step_path() == "split"
+        resets += int(outs[0].reset_mask.sum())
+        _same(outs, t)
+        assert torch.equal(outs[0].action_mask, outs[1].action_mask), t
+    s0, s1 = single.export_state(), split.export_state()
+    for k in s0:
+        assert torch.equal(s0[k], s1[k]), k
+    if scen == "c1_3v3":
+        assert resets > 0  # auto-resets happened inside the single kernel
+
+
+def test_single_launch_step_matches_oracle(monkeypatch):
+    """C1 (the BASELINE parity config, 256 envs) through the single-launch step
+    against the oracle for 120 steps, auto-resets included."""
+    monkeypatch.setenv("TABX_NO_K0", "1")
+    sc = builtin_scenario("c1_3v3").scripted()
+    B = 256
+    seeds = np.arange(B, dtype=np.uint64) + 900
+    gpu = BatchSim([sc] * B, seeds, auto_reset=True, device="cuda:0")
+    ora = orc.OracleBatchSim([sc] * B, seeds, auto_reset=True)
+    for t in range(120):
+        g = gpu.step(None)
+        assert gpu.step_path() == "single"
+        o = ora.step(None)
+        bad = compare_outputs(g, o, f"single t={t}")
+        if t % 10 == 9:
+            bad += compare_state(gpu.export_state(), ora.sim, f"single t={t}")
+        assert not bad, "\n".join(bad[:10])
+    gpu.close()
