@@ -223,10 +223,19 @@ class Ctx:
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
         self.rank, self.world, self.local = dist_env()
+        # TABX_BENCH_SHARED_GPU=1: a control-flow dry run of the N > 1 path on
+        # one GPU (every rank on cuda:0, gloo for the collectives); its timings
+        # mean nothing -- the real N > 1 run is one rank per GPU over NCCL
+        shared = os.environ.get("TABX_BENCH_SHARED_GPU") == "1"
+        if shared:
+            self.local = 0
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         if self.world > 1:
-            dist.init_process_group("nccl", device_id=self.dev)
+            if shared:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=self.dev)
         self.stream = torch.cuda.current_stream(self.dev)
 
     def barrier(self):

@@ -46,7 +46,7 @@ SELECT = ("test_golden_case_parity or test_injected_state_single_step or "
           "test_mixed_configs_and_reset_env_swap or test_controller_pass_mixed_heuristic_counts "
           "or test_action_mask_error or test_dead_units or test_fov_boundary or "
           "test_slot_recycling or test_batch_of_levels_and_respawn or "
-          "test_fused_small_and_ragged_batches_match_oracle")
+          "test_fused_small_and_ragged_batches_match_oracle or test_single_launch_step_matches_oracle")
 
 
 def test_parity_cases_through_checked_kernels():
