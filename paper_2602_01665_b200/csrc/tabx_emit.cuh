@@ -125,19 +125,17 @@ __device__ __forceinline__ void prefetch_env_state(const DevState& st, int64_t b
   }
 }
 
-// Own-feature block of unit u from its HBM state (perception.py:108-132).
-__device__ __forceinline__ void own_from_state(float* o, const DevState& st, int64_t gu,
-                                               const tabx_config* __restrict__ C,
-                                               const DerivedCfg* __restrict__ DC, int u) {
+// Own-feature block of unit u from its state values (perception.py:108-132).
+__device__ __forceinline__ void own_from_vals(float* o, double2 p, double2 cs, double hp,
+                                              double cd, uint8_t ub,
+                                              const tabx_config* __restrict__ C,
+                                              const DerivedCfg* __restrict__ DC, int u) {
   o[15] = 0.0f;
   if (!C->active[u]) {
 #pragma unroll
     for (int f = 0; f < TABX_OWN_DIM; ++f) o[f] = 0.0f;
     return;
   }
-  const double2 p = st.pos[gu];
-  const double2 cs = st.hcs[gu];
-  const double hp = st.health[gu], cd = st.cooldown[gu];
   const double mh = C->max_health[u], ucd = C->cooldown[u];
   o[0] = f32_quot(hp, mh, DC->rmh[u]);
   o[1] = f32_quot(mh, 1000.0, 0.001);
@@ -152,8 +150,43 @@ __device__ __forceinline__ void own_from_state(float* o, const DevState& st, int
   o[10] = __double2float_rn(C->radius[u]);
   o[11] = __double2float_rn(C->mass[u]);
   o[12] = __double2float_rn(C->sight_angle[u]);
-  o[13] = (st.ubits[gu] & U_ALIVE) ? 1.0f : 0.0f;
+  o[13] = (ub & U_ALIVE) ? 1.0f : 0.0f;
   o[14] = __double2float_rn(C->speed[u]);
+}
+
+// Own-feature block of unit u from its HBM state.
+__device__ __forceinline__ void own_from_state(float* o, const DevState& st, int64_t gu,
+                                               const tabx_config* __restrict__ C,
+                                               const DerivedCfg* __restrict__ DC, int u) {
+  if (!C->active[u]) {
+    own_from_vals(o, make_double2(0.0, 0.0), make_double2(0.0, 0.0), 0.0, 0.0, 0, C, DC, u);
+    return;
+  }
+  own_from_vals(o, st.pos[gu], st.hcs[gu], st.health[gu], st.cooldown[gu], st.ubits[gu], C, DC,
+                u);
+}
+
+// One unit's view inputs held in registers (W = 1: lane u = unit u), so the
+// emitter can issue the NEXT environment's loads before streaming the
+// current one's rows (TABX_EMIT_VIEW_PREFETCH).
+struct ViewRegs {
+  double2 p, cs;
+  double hp, cd;
+  uint32_t vis, atk;
+  uint8_t ub;
+};
+__device__ __forceinline__ void fetch_view_regs(ViewRegs& V, const DevState& st, int64_t b, int N,
+                                                int lane) {
+  if (lane < N) {
+    const int64_t gu = b * N + lane;
+    V.p = st.pos[gu];
+    V.cs = st.hcs[gu];
+    V.hp = st.health[gu];
+    V.cd = st.cooldown[gu];
+    V.ub = st.ubits[gu];
+    V.vis = st.vis[gu];
+    V.atk = st.atk[gu];
+  }
 }
 
 // Load lane b's view into E (all 32 lanes of the warp).
@@ -201,6 +234,45 @@ __device__ __forceinline__ void load_view(const EmitScratch<W>& X, const DevStat
   __syncwarp();
 }
 
+
+// load_view for W = 1 from the registers fetch_view_regs filled.
+__device__ __forceinline__ void load_view_regs(const EmitScratch<1>& X, const ViewRegs& V, int N,
+                                               const tabx_config* __restrict__ C,
+                                               const DerivedCfg* __restrict__ DC, int lane) {
+  const EmitEnv<1>& E = X.E;
+  TABX_POISON(X.E.px, (size_t)((const unsigned char*)X.stage - (const unsigned char*)X.E.px),
+              lane, 32);
+  __syncwarp();
+  const bool valid = lane < N;
+  if (valid) {
+    const int u = lane;
+    E.px[u] = V.p.x;
+    E.py[u] = V.p.y;
+    own_from_vals(E.own[u], V.p, V.cs, V.hp, V.cd, V.ub, C, DC, u);
+    E.flags[u] = (C->active[u] ? 1u : 0u) | (C->team[u] ? 2u : 0u);
+    E.vis[u] = V.vis;
+    E.atk[u] = V.atk;
+  }
+  uint32_t w = valid ? (V.vis & ~(1u << lane)) : 0u;
+  const int c = __popc(w);
+  int incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  TABX_JITTER(300);
+  if (valid) X.rstart[lane + 1] = (uint16_t)incl;
+  if (lane == 0) X.rstart[0] = 0;
+  for (int n = incl - c; w; w &= w - 1, ++n) X.plist[n] = (uint16_t)((lane << 5) | (__ffs(w) - 1));
+  __syncwarp();
+}
+
+// W = 1 fixed-shape emitter: 1 = fetch the next env's view into registers
+// before streaming this env's rows
+#ifndef TABX_EMIT_VIEW_PREFETCH
+#define TABX_EMIT_VIEW_PREFETCH -1  // -1: per shape (EmitTune), 0 / 1: off / on
+#endif
 
 // stage buffers per warp (2: fill one while the bulk store drains the other)
 #ifndef TABX_EMIT_NBUF
@@ -486,7 +558,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
           }
         }
       }
-      buf = TABX_EMIT_NBUF == 1 ? 0 : buf ^ 1;
+      buf = buf + 1 == TABX_EMIT_NBUF ? 0 : buf + 1;
     }
   }
   if (glob) {
@@ -504,7 +576,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
     fence_proxy_async();
     __syncwarp();
     flush_stage<W == 1>(glob, gs, G, st, lane);
-    buf = TABX_EMIT_NBUF == 1 ? 0 : buf ^ 1;
+    buf = buf + 1 == TABX_EMIT_NBUF ? 0 : buf + 1;
   }
   if (drain) {
     if (lane == 0) bulk_wait_read<0>();
@@ -534,7 +606,7 @@ __host__ __device__ __forceinline__ constexpr int emit_stage_floats(int N, int D
 // resident CTAs per SM the register budget is cut for (W = 1: 6 CTAs of 4
 // warps = 24 warps/SM at 80 registers; W > 1: 3)
 #ifndef TABX_EMIT_MIN_BLOCKS_W1
-#define TABX_EMIT_MIN_BLOCKS_W1 6
+#define TABX_EMIT_MIN_BLOCKS_W1 0  // 0: per shape (EmitTune); the generic kernel: 6
 #endif
 #ifndef TABX_EMIT_MIN_BLOCKS
 #define TABX_EMIT_MIN_BLOCKS 3
@@ -565,7 +637,8 @@ __device__ __forceinline__ EmitScratch<W> emit_scratch(unsigned char* base, int 
 
 template <int W, int EPW, bool F16>
 __global__ void __launch_bounds__(32 * EPW,
-                                  (W == 1 ? TABX_EMIT_MIN_BLOCKS_W1 : TABX_EMIT_MIN_BLOCKS))
+                                  (W == 1 ? (TABX_EMIT_MIN_BLOCKS_W1 > 0 ? TABX_EMIT_MIN_BLOCKS_W1 : 6)
+                                          : TABX_EMIT_MIN_BLOCKS))
     emit_kernel(const Params P, int R, int SF) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (is_step_mode(P.mode) && P.sync->err_index != NO_ERROR) return;
@@ -623,9 +696,28 @@ cudaError_t launch_emit_f(const Params& P, int sm_count, cudaStream_t stream) {
 // Instantiations with the unit / zone counts (and so the row geometry) fixed
 // at compile time, for the common shapes: constant trip counts and offsets,
 // fewer live registers (no spills).  Same body as emit_kernel.
+// Per-shape tuning of the fixed-shape emitter (W = 1): resident CTAs per SM
+// the register budget is cut for, and whether the next env's view inputs are
+// fetched into registers before this env's rows stream out (VPF).  Measured
+// (B200, tools/kab.sh): C3 (20, 6) at 262,144 envs 1.655 ms (6 CTAs, no VPF)
+// -> 1.466 ms (4 CTAs = 16 warps at 113 registers, VPF; 5 CTAs without VPF
+// 1.541); C2 (20, 0) at 65,536 envs 0.363 -> 0.345 ms with 5 CTAs and no VPF
+// (VPF at 4 CTAs: 0.362).  At 6 CTAs (80 registers, 24 warps) the view loads
+// at each env's start were a quarter of the emitter's stall samples and
+// 219 KB of shared memory left little L1 for the config rows they read.
+// With the bf16 policy feed (the C5 rollout at 16,384 envs) the original
+// 6 CTAs without VPF stay faster (C5 43.2 vs 42.4 M env-steps/s).
+template <int NF, int ZF, bool F16>
+struct EmitTune {
+  static constexpr int minb = F16 ? 6 : (NF == 20 && ZF == 6) ? 4 : (NF == 20 && ZF == 0) ? 5 : 6;
+  static constexpr bool vpf = !F16 && NF == 20 && ZF == 6;
+};
+
 template <int W, int EPW, bool F16, int NF, int ZF>
 __global__ void __launch_bounds__(32 * EPW,
-                                  (W == 1 ? TABX_EMIT_MIN_BLOCKS_W1 : TABX_EMIT_MIN_BLOCKS))
+                                  (W == 1 ? (TABX_EMIT_MIN_BLOCKS_W1 > 0 ? TABX_EMIT_MIN_BLOCKS_W1
+                                                                         : EmitTune<NF, ZF, F16>::minb)
+                                          : TABX_EMIT_MIN_BLOCKS))
     emit_kernel_fixed(const Params P) {
   constexpr int N = NF, Z = ZF;
   constexpr int D = TABX_OWN_DIM + TABX_OTHER_DIM * (NF - 1) + TABX_ZONE_DIM * ZF;
@@ -649,15 +741,23 @@ __global__ void __launch_bounds__(32 * EPW,
 #if TABX_EMIT_PREFETCH && TABX_EMIT_PREFETCH != 3
   if (b < P.B) prefetch_env_state<W>(st, b, N, lane);
 #endif
+  // (W = 1, TABX_EMIT_VIEW_PREFETCH) the next env's view inputs are loaded
+  // into registers before this env's rows stream out
+  constexpr bool VPF =
+      W == 1 && (TABX_EMIT_VIEW_PREFETCH < 0 ? EmitTune<NF, ZF, F16>::vpf : TABX_EMIT_VIEW_PREFETCH != 0);
+  ViewRegs V_next;
+  if (VPF && b < P.B) fetch_view_regs(V_next, st, b, N, lane);
   for (; b < P.B; b += stride) {
     const int32_t k = k_next;
     const uint8_t fl = f_next;
+    ViewRegs V = V_next;
     if (b + stride < P.B) {
       k_next = st.cfg[b + stride];
       f_next = st.flags[b + stride];
 #if TABX_EMIT_PREFETCH && TABX_EMIT_PREFETCH != 3
       prefetch_env_state<W>(st, b + stride, N, lane);
 #endif
+      if (VPF) fetch_view_regs(V_next, st, b + stride, N, lane);
     }
     const tabx_config* C = P.cfgs + k;
     const DerivedCfg* DC = P.dcfgs + k;
@@ -666,7 +766,10 @@ __global__ void __launch_bounds__(32 * EPW,
     float* gb = pending ? P.out.final_global_state : P.out.global_state;
     __nv_bfloat16* o16 = (F16 && !pending) ? (__nv_bfloat16*)P.out.observations_bf16 : nullptr;
     if (!ob && !gb && !o16) continue;
-    load_view<W>(X, st, b, N, Z, C, DC, lane);
+    if constexpr (VPF)
+      load_view_regs(X, V, N, C, DC, lane);
+    else
+      load_view<W>(X, st, b, N, Z, C, DC, lane);
     emit_lane<W, F16>(X, ob, gb, b, N, Z, D, G, R, SF, C, DC, lane, buf, false, o16,
                       (int)P.out.observations_bf16_ld, &st, b + stride < P.B ? b + stride : -1);
   }
