@@ -282,14 +282,20 @@ static void move_lane(tabx_handle* h, int64_t b, int32_t k) {
   }
 }
 
+// The pinned staging ring for config rows (tabx_reset_env).  Allocated at
+// creation: a page-locked allocation can take ~100 ms, which on first use
+// made the first new-config reset_env the protocol's worst case.
+static cudaError_t alloc_stage(tabx_handle* h) {
+  if (h->stage) return cudaSuccess;
+  cudaError_t e = cudaHostAlloc((void**)&h->stage, sizeof(tabx_config) * tabx_handle::STAGE_SLOTS,
+                                cudaHostAllocDefault);
+  for (int q = 0; e == cudaSuccess && q < tabx_handle::STAGE_SLOTS; ++q)
+    e = cudaEventCreateWithFlags(&h->stage_ev[q], cudaEventDisableTiming);
+  return e;
+}
+
 static int stage_config(tabx_handle* h, const tabx_config* c, const tabx_config** staged) {
-  if (!h->stage) {
-    TABX_CUDA(cudaHostAlloc((void**)&h->stage, sizeof(tabx_config) * tabx_handle::STAGE_SLOTS,
-                            cudaHostAllocDefault),
-              "config staging allocation");
-    for (int q = 0; q < tabx_handle::STAGE_SLOTS; ++q)
-      TABX_CUDA(cudaEventCreateWithFlags(&h->stage_ev[q], cudaEventDisableTiming), "event create");
-  }
+  TABX_CUDA(alloc_stage(h), "config staging allocation");
   const int q = h->stage_next;
   h->stage_next = (q + 1) % tabx_handle::STAGE_SLOTS;
   // the copy that last used this staging row must have read it (normally
@@ -504,9 +510,15 @@ int tabx_create(const tabx_config* configs, int32_t n_configs, const int32_t* en
   if (e == cudaSuccess) e = cudaMemsetAsync(&h->sync->err_index, 0xFF, 8, h->stream);
   if (e == cudaSuccess)
     e = launch_spawn(st, h->cfg_dev, h->dcfg_dev, 0, B, N, (int)W, 1, h->sm_count, h->stream);
+  if (e == cudaSuccess) e = alloc_stage(h);
   if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);  // host arrays may be freed
   if (e != cudaSuccess) {
     rc = cuda_fail(e, "tabx_create");
+    if (h->stage) {
+      for (int q = 0; q < tabx_handle::STAGE_SLOTS; ++q)
+        if (h->stage_ev[q]) cudaEventDestroy(h->stage_ev[q]);
+      cudaFreeHost(h->stage);
+    }
     cudaFree(h->dcfg_dev);
     cudaFree(h->cfg_dev);
     cudaFree(h->arena);
