@@ -1514,11 +1514,14 @@ struct CtrlView {
   uint32_t m_active[W], m_alive[W];
 };
 
+// K0 resident CTAs per SM the register budget is cut for: W = 1 6 (80
+// registers; 4 and 5 measured neutral at C3), W > 1 4 (128 registers; C4
+// refresh + K0 + K1 7.18 -> 7.05 ms)
 #ifndef TABX_K0_MINB
-#define TABX_K0_MINB 6
+#define TABX_K0_MINB(W) ((W) == 1 ? 6 : 4)
 #endif
 template <int W>
-__global__ void __launch_bounds__(128, TABX_K0_MINB) ctrl_kernel(const Params P, int G, int NH) {
+__global__ void __launch_bounds__(128, TABX_K0_MINB(W)) ctrl_kernel(const Params P, int G, int NH) {
   if (P.sync->err_index != NO_ERROR) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
