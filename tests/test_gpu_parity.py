@@ -112,7 +112,12 @@ def test_injected_state_single_step(scen, B, seed):
         assert not bad, "\n".join(bad[:10])
 
 
-def test_action_mask_error_matches_reference_and_mutates_nothing():
+@pytest.mark.parametrize("path", ["k0", "single"])
+def test_action_mask_error_matches_reference_and_mutates_nothing(path, monkeypatch):
+    """path k0: controller pass + step kernels; single: the small-batch
+    single-launch step (in-kernel controller, TABX_NO_K0=1)."""
+    if path == "single":
+        monkeypatch.setenv("TABX_NO_K0", "1")
     sc = builtin_scenario("c2_10v10")  # ally external
     B = 4
     seeds = np.arange(B, dtype=np.uint64)
@@ -136,6 +141,7 @@ def test_action_mask_error_matches_reference_and_mutates_nothing():
     # the simulator keeps working after the error
     o = ora.step(acts)
     g = gpu.step(acts)
+    assert gpu.step_path() == ("single" if path == "single" else "split")
     assert not compare_outputs(g, o, "after error")
 
 
