@@ -72,16 +72,22 @@ __global__ void validate_kernel(const int64_t* __restrict__ actions, DevState st
        u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = u / N;
     const int i = (int)(u - b * N);
-    if (st.flags[b] & F_DONE) continue;
-    const tabx_config* C = cfgs + st.cfg[b];
-    if (!C->active[i] || !(st.ubits[u] & U_ALIVE)) continue;
-    if (C->controller[C->team[i] ? 1 : 0] != TABX_CTRL_EXTERNAL) continue;
+    // every input issued before the first test: one DRAM round trip per
+    // unit instead of a chain of dependent ones behind early exits
+    const uint8_t fl = st.flags[b];
+    const int32_t k = st.cfg[b];
+    const uint8_t ub = st.ubits[u];
     const int64_t a = actions[u];
+    const double cd = st.cooldown[u];
+    const tabx_config* C = cfgs + k;
+    const bool ext = !(fl & F_DONE) && C->active[i] && (ub & U_ALIVE) &&
+                     C->controller[C->team[i] ? 1 : 0] == TABX_CTRL_EXTERNAL;
+    if (!ext) continue;
     bool ok;
     if (a < 0 || a >= TABX_NUM_ACTIONS) {
       ok = false;
     } else if (a == A_ATTACK) {
-      ok = st.cooldown[u] <= 0.0;
+      ok = cd <= 0.0;
     } else if (a == A_NOOP) {
       ok = C->enable_noop != 0;
     } else {
