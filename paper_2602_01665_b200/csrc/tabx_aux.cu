@@ -299,6 +299,10 @@ __global__ void derive_kernel(const tabx_config* __restrict__ cfgs, DerivedCfg* 
     }
     if (threadIdx.x == 0) {
       D->rw = 1.0 / C->field_w;
+      double rmx = 0.0;
+      for (int i = 0; i < C->n_units; ++i)
+        if (C->active[i] && C->radius[i] > rmx) rmx = C->radius[i];
+      D->rad_max = rmx;
       D->rh = 1.0 / C->field_h;
       uint32_t lm = 0, bm = 0, sm = 0;
       for (int z = 0; z < C->n_zones; ++z) {

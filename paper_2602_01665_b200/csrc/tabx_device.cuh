@@ -133,6 +133,7 @@ struct Sync {
 // reciprocals for the fast exact-rounding paths, float copies for filters.
 struct DerivedCfg {
   double rw, rh;                      // 1/field_w, 1/field_h
+  double rad_max;                     // largest radius of an active unit (contact sweep window)
   double rax[TABX_MAX_ZONES], ray[TABX_MAX_ZONES];
   double rmh[TABX_MAX_UNITS];         // 1/max_health
   double rucd[TABX_MAX_UNITS];        // 1/cooldown (0 if cooldown == 0)

@@ -80,6 +80,14 @@ __device__ __forceinline__ double uniform53(uint64_t seed, uint64_t step, uint64
 #define TABX_PAIR_CONTACTS 1
 #endif
 
+// W > 1: cull the O(N^2) contact and visibility pair passes with a sort of
+// the units along y and a sweep over the |dy| window:
+// a pair with |dy| beyond the window cannot touch / be in sight, since the
+// reference's float64 distance is never below |dy|
+#ifndef TABX_SWEEP
+#define TABX_SWEEP 1
+#endif
+
 // ------------------------------------------------------------- helpers --
 constexpr uint32_t UF_ACTIVE = 1, UF_ALIVE = 2, UF_ENEMY = 4, UF_KIN = 8, UF_INJURED = 16;
 
@@ -89,6 +97,11 @@ struct EnvSmem {
   double px[NT], py[NT], ch[NT], sh[NT], rad[NT], mh[NT], rv[NT], dmg[NT];
   double vx[NT], vy[NT], sx[NT], sy[NT];
   uint32_t vis[NT * W], atk[NT * W], touch[NT * W];
+  // W > 1 sort-and-sweep culling: float32 y keys (+inf for inactive units),
+  // the units in ascending key order and each unit's rank in it
+  float ykey[NT];
+  int16_t ord[NT], rnk[NT];
+  uint32_t dymax;  // float bits: largest |y| move since the keys were taken
   uint32_t uf[NT];
   uint32_t zin[NT];
   int32_t tgt[NT];
@@ -146,6 +159,30 @@ __device__ __forceinline__ int env_count(bool p, EnvSmem<W>& S, int i) {
 #pragma unroll
   for (int k = 0; k < W; ++k) c += __popc(m[k]);
   return c;
+}
+
+// Rank of every unit by its published y key (ties by index), all threads:
+// S.ord[rank] = unit, S.rnk[unit] = rank.  Barrier-free O(N) per thread.
+template <int W>
+__device__ __forceinline__ void rank_by_y(EnvSmem<W>& S, int i, int N) {
+  if (i < N) {
+    const float ki = S.ykey[i];
+    int r = 0;
+    for (int j = 0; j < N; ++j) {
+      const float kj = S.ykey[j];
+      r += (kj < ki) | ((kj == ki) & (j < i));
+    }
+    S.ord[r] = (int16_t)i;
+    S.rnk[i] = (int16_t)r;
+  }
+}
+
+// Upper bound of |dy| - (key_j - key_i) for keys within `win` of key_i:
+// the keys are float32 roundings of float64 ys (relative error 2^-24 each)
+// and their difference rounds once more; 2^-21 leaves an 8x margin.
+__device__ __forceinline__ float sweep_limit(float yi, double win) {
+  const float w = (float)win;
+  return w + (2.0f * fabsf(yi) + 2.0f * w) * 0x1p-21f + 1e-30f;
 }
 
 // Env-wide unit masks from the per-unit state just published (all threads).
@@ -339,7 +376,7 @@ static __device__ __noinline__ bool exact_box(double dx, double dy, double ch, d
 // env-wide masks, and the strike box + exact distance (which orders the
 // target) run only over the few attackable candidates.  Verdicts are exactly
 // the float64 ones.
-template <int W>
+template <int W, bool SWEEP = false>
 __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, double cos_half,
                                               double srange, double dmg, double reach, double rad,
                                               uint32_t bush_m) {
@@ -359,8 +396,24 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
     uint32_t seen[W], unsure[W];
 #pragma unroll
     for (int k = 0; k < W; ++k) seen[k] = unsure[k] = 0u;
+    // SWEEP (W > 1, ranks of this stage's positions in S): only the units
+    // whose y key lies within the sight range of this one's, a contiguous
+    // run of the y order around its rank; every other unit has |dy| >
+    // srange and so dist > srange (not seen)
+    int q0 = 0, q1 = N;
+    if constexpr (SWEEP) {
+      // keys and order of the contact pass; every unit moved by at most dymax
+      const float yi = S.ykey[i];
+      const float lim = sweep_limit(yi, srange + 2.0 * (double)__uint_as_float(S.dymax));
+      const int r = S.rnk[i];
+      q0 = r;
+      while (q0 > 0 && yi - S.ykey[S.ord[q0 - 1]] <= lim) --q0;
+      q1 = r + 1;
+      while (q1 < N && S.ykey[S.ord[q1]] - yi <= lim) ++q1;
+    }
 #pragma unroll 4
-    for (int j = 0; j < N; ++j) {
+    for (int q = q0; q < q1; ++q) {
+      const int j = SWEEP ? (int)S.ord[q] : q;
       const float dxf = (float)(S.px[j] - px), dyf = (float)(S.py[j] - py);
       const float d2f = dxf * dxf + dyf * dyf;
       const float cdevf = (dxf * chf + dyf * shf) * rsqrt_approx(d2f);
@@ -479,7 +532,8 @@ __device__ __forceinline__ int cache_row_of(EnvSmem<W>& S, int i, int N, const U
 template <int W>
 __device__ __forceinline__ int cache_row_inl(EnvSmem<W>& S, int i, int N, const UnitStatic& U,
                                              uint32_t bush_m) {
-  return cache_row_body<W>(S, i, N, U.cos_half, U.srange, U.dmg, U.range, U.rad, bush_m);
+  return cache_row_body<W, (W > 1 && TABX_SWEEP)>(S, i, N, U.cos_half, U.srange, U.dmg, U.range,
+                                                   U.rad, bush_m);
 }
 
 // Team health ratio sums in numpy pairwise order (arrays.py:390-400); one
@@ -997,7 +1051,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const double tick = (U.active && running) ? dt : 0.0;
   cd = np_max(cd - tick, 0.0);
   rv = np_max(rv - tick, 0.0);
-  if (W > 1 && TABX_PAIR_CONTACTS) {  // this step's touching rows (read after the barriers below)
+  if (W > 1 && (TABX_PAIR_CONTACTS || TABX_SWEEP)) {  // this step's touching rows (read after the barriers below)
 #pragma unroll
     for (int k = 0; k < W; ++k) S.touch[i * W + k] = 0u;
   }
@@ -1010,10 +1064,19 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
 #endif
   S.px[i] = px;
   S.py[i] = py;
+  const double py_key = py;  // y the sweep keys are taken at
+  if (W > 1 && TABX_SWEEP) {
+    S.ykey[i] = (valid && U.active) ? (float)py : __int_as_float(0x7f800000);
+    if (i == 0) S.dymax = 0u;
+  }
 #ifdef TABX_SELFTEST_RACE  // negative control of the checked build: W > 1 hand-off without its barrier
   if (W == 1)
 #endif
   env_sync<W>();
+  if (W > 1 && TABX_SWEEP) {
+    rank_by_y<W>(S, i, N);
+    env_sync<W>();
+  }
 
   // 5. contacts: detection (physics.py:27-49), Gauss-Seidel (physics.py:52-94)
   // float32 filter on squared distance vs rs^2 (margin 1e-5 relative);
@@ -1054,6 +1117,41 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
       anyw |= bm;
     }
     any_touch = anyw != 0u;
+  } else if (TABX_SWEEP) {
+    // each active unit scans forward in y order while the key gap is within
+    // the largest contact distance 2 rad_max; every unordered pair with
+    // |dy| <= 2 rad_max is seen once (from its lower-ranked unit); a hit sets
+    // bit c of row a in S.touch (rows were cleared before the hand-off)
+    if (running && valid && U.active) {
+      const float yi = S.ykey[i];
+      const float lim = sweep_limit(yi, 2.0 * DC->rad_max);
+      for (int q = S.rnk[i] + 1; q < N; ++q) {
+        const int j = S.ord[q];
+        if (!(S.ykey[j] - yi <= lim)) break;  // ascending keys (+inf last)
+        const int a = i < j ? i : j, c = i < j ? j : i;
+        const double dx = S.px[c] - S.px[a], dy = S.py[c] - S.py[a];
+        const double rs = S.rad[a] + S.rad[c];
+        const float dxf = (float)dx, dyf = (float)dy;
+        const float d2f = dxf * dxf + dyf * dyf;
+        const float rs2f = (float)(rs * rs);
+        bool hit = false;
+        if (d2f < rs2f * 0.99999f && d2f > 1e-30f) {
+          hit = true;
+        } else if (!(d2f > rs2f * 1.00001f)) {
+          TABX_COUNT(3);
+          const double dist = slow_sqrt(dx * dx + dy * dy);
+          hit = (dist == 0.0 ? rs : rs - dist) > 0.0;
+        }
+        if (hit) atomicOr(&S.touch[a * W + (c >> 5)], 1u << (c & 31));
+      }
+    }
+    env_sync<W>();
+    bool mine = false;
+#pragma unroll
+    for (int k = 0; k < W; ++k) mine |= S.touch[i * W + k] != 0u;
+    env_ballot<W>(mine, S, i, rowm);
+#pragma unroll
+    for (int k = 0; k < W; ++k) any_touch |= rowm[k] != 0u;
   } else if (TABX_PAIR_CONTACTS) {
     // all 32 W threads over the N(N-1)/2 unordered pairs (a < c, row-major),
     // each a contiguous range of ceil(NP / 32 W) pairs, so the detection is
@@ -1244,6 +1342,12 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   TABX_PHASE(12);
   env_sync<W>();
   publish();
+  if (W > 1 && TABX_SWEEP && valid && U.active) {
+    // the y order of the contact pass stands; windows widen by twice the
+    // largest move since (contact correction, boundary clip), rounded up
+    const float d = (float)fabs(py - py_key) * (1.0f + 0x1p-20f);
+    if (d > 0.0f) atomicMax(&S.dymax, __float_as_uint(d));
+  }
   build_masks<W>(S, i, valid, U.active, alive, U.enemy, rv, zin, Z, bush_m);
   env_sync<W>();
   TABX_PHASE(13);
