@@ -99,8 +99,10 @@ struct EnvSmem {
   uint32_t vis[NT * W], atk[NT * W], touch[NT * W];
   // W > 1 sort-and-sweep culling: float32 y keys (+inf for inactive units),
   // the units in ascending key order and each unit's rank in it
-  float ykey[NT];
+  float ykey[NT], skey[NT];  // skey[r] = key of the unit of rank r
   int16_t ord[NT], rnk[NT];
+  float rk_key[NT];  // per-warp sorted runs (rank_by_y)
+  int16_t rk_id[NT];
   uint32_t dymax;  // float bits: largest |y| move since the keys were taken
   uint32_t uf[NT];
   uint32_t zin[NT];
@@ -162,19 +164,79 @@ __device__ __forceinline__ int env_count(bool p, EnvSmem<W>& S, int i) {
 }
 
 // Rank of every unit by its published y key (ties by index), all threads:
-// S.ord[rank] = unit, S.rnk[unit] = rank.  Barrier-free O(N) per thread.
+// S.ord[rank] = unit, S.rnk[unit] = rank, S.skey[rank] = key.  Each warp
+// sorts its 32 (key, index) pairs with a shuffle bitonic network, then every
+// element's rank is its place in its run plus the number of smaller
+// elements in each other warp's run (binary searches); one barrier.
 template <int W>
 __device__ __forceinline__ void rank_by_y(EnvSmem<W>& S, int i, int N) {
-  if (i < N) {
-    const float ki = S.ykey[i];
-    int r = 0;
-    for (int j = 0; j < N; ++j) {
-      const float kj = S.ykey[j];
-      r += (kj < ki) | ((kj == ki) & (j < i));
+  const uint32_t full = 0xffffffffu;
+  const int lane = i & 31, w = i >> 5;
+  float k = S.ykey[i];  // +inf for inactive units and threads past N
+  int id = i;
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const float ok = __shfl_xor_sync(full, k, stride);
+      const int oid = __shfl_xor_sync(full, id, stride);
+      const bool up = (lane & size) == 0;
+      const bool lower = (lane & stride) == 0;
+      const bool o_less = (ok < k) || (ok == k && oid < id);
+      const bool take = lower ? (up ? o_less : !o_less) : (up ? !o_less : o_less);
+      if (take) {
+        k = ok;
+        id = oid;
+      }
     }
-    S.ord[r] = (int16_t)i;
-    S.rnk[i] = (int16_t)r;
   }
+  S.rk_key[i] = k;
+  S.rk_id[i] = (int16_t)id;
+  env_sync<W>();
+  int r = lane;
+#pragma unroll
+  for (int w2 = 0; w2 < W; ++w2) {
+    if (w2 == w) continue;
+    const float* rk = S.rk_key + w2 * 32;
+    const int16_t* ri = S.rk_id + w2 * 32;
+    int lo = 0, hi = 32;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const float kk = rk[mid];
+      if (kk < k || (kk == k && ri[mid] < id)) lo = mid + 1; else hi = mid;
+    }
+    r += lo;
+  }
+#ifdef TABX_SELFTEST_RACE
+  // negative control: half the threads publish their ranks 20 us late
+  if ((threadIdx.x * 0x9E3779B9u) >> 31) __nanosleep(20000);
+#endif
+  if (id < N) {
+    S.ord[r] = (int16_t)id;
+    S.rnk[id] = (int16_t)r;
+    S.skey[r] = k;
+  }
+}
+
+// First rank in [0, N) whose sorted key is >= v (N if none).
+template <int W>
+__device__ __forceinline__ int lower_rank(const EnvSmem<W>& S, int N, float v) {
+  int lo = 0, hi = N;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (S.skey[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+// First rank in [0, N) whose sorted key is > v (N if none).
+template <int W>
+__device__ __forceinline__ int upper_rank(const EnvSmem<W>& S, int N, float v) {
+  int lo = 0, hi = N;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (S.skey[mid] <= v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
 }
 
 // Upper bound of |dy| - (key_j - key_i) for keys within `win` of key_i:
@@ -190,27 +252,26 @@ template <int W>
 __device__ __forceinline__ void build_masks(EnvSmem<W>& S, int i, bool valid, bool active,
                                             bool alive, bool enemy, double rv, uint32_t zin,
                                             int Z, uint32_t bush_m) {
-  uint32_t m[W];
-  env_ballot<W>(valid && active, S, i, m);
-  if ((i & 31) == 0) S.m_active[i >> 5] = m[i >> 5];
-  env_ballot<W>(valid && alive, S, i, m);
-  if ((i & 31) == 0) S.m_alive[i >> 5] = m[i >> 5];
-  env_ballot<W>(valid && enemy, S, i, m);
-  if ((i & 31) == 0) S.m_enemy[i >> 5] = m[i >> 5];
-  env_ballot<W>(valid && rv > 0.0, S, i, m);
-  if ((i & 31) == 0) S.m_rev[i >> 5] = m[i >> 5];
-  uint32_t inb[W];
-#pragma unroll
-  for (int k = 0; k < W; ++k) inb[k] = 0u;
+  // word k of every mask is warp k's ballot: each warp writes its own words
+  // (no cross-warp exchange here; the caller's barrier publishes them)
+  const uint32_t full = 0xffffffffu;
+  const uint32_t ma = __ballot_sync(full, valid && active);
+  const uint32_t ml = __ballot_sync(full, valid && alive);
+  const uint32_t me = __ballot_sync(full, valid && enemy);
+  const uint32_t mr = __ballot_sync(full, valid && rv > 0.0);
+  uint32_t inb = 0u;
   for (int z = 0; z < Z; ++z) {
-    env_ballot<W>(valid && ((zin >> z) & 1u), S, i, m);
-    if ((i & 31) == 0) S.m_zone[z][i >> 5] = m[i >> 5];
-    if ((bush_m >> z) & 1u) {
-#pragma unroll
-      for (int k = 0; k < W; ++k) inb[k] |= m[k];
-    }
+    const uint32_t mz = __ballot_sync(full, valid && ((zin >> z) & 1u));
+    if ((i & 31) == 0) S.m_zone[z][i >> 5] = mz;
+    if ((bush_m >> z) & 1u) inb |= mz;
   }
-  if ((i & 31) == 0) S.m_inbush[i >> 5] = inb[i >> 5];
+  if ((i & 31) == 0) {
+    S.m_active[i >> 5] = ma;
+    S.m_alive[i >> 5] = ml;
+    S.m_enemy[i >> 5] = me;
+    S.m_rev[i >> 5] = mr;
+    S.m_inbush[i >> 5] = inb;
+  }
 }
 
 __device__ __forceinline__ bool bit_of(const uint32_t* row, int j) {
@@ -405,11 +466,11 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
       // keys and order of the contact pass; every unit moved by at most dymax
       const float yi = S.ykey[i];
       const float lim = sweep_limit(yi, srange + 2.0 * (double)__uint_as_float(S.dymax));
-      const int r = S.rnk[i];
-      q0 = r;
-      while (q0 > 0 && yi - S.ykey[S.ord[q0 - 1]] <= lim) --q0;
-      q1 = r + 1;
-      while (q1 < N && S.ykey[S.ord[q1]] - yi <= lim) ++q1;
+      // keys k with |k - yi| <= lim: ranks [q0, q1) (binary searches; the
+      // float bounds yi -+ lim round outward by at most an ulp, covered by
+      // lim's margin)
+      q0 = lower_rank<W>(S, N, yi - lim);
+      q1 = upper_rank<W>(S, N, yi + lim);
     }
 #pragma unroll 4
     for (int q = q0; q < q1; ++q) {
@@ -1057,11 +1118,6 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   }
   env_sync<W>();
   TABX_JITTER(200);  // (checked build) publish the new positions out of step
-#ifdef TABX_SELFTEST_RACE
-  // negative control: half the threads publish 20 us late, past the
-  // contact filter's and the exact fallback's reads of the positions
-  if ((threadIdx.x * 0x9E3779B9u) >> 31) __nanosleep(20000);
-#endif
   S.px[i] = px;
   S.py[i] = py;
   const double py_key = py;  // y the sweep keys are taken at
@@ -1069,12 +1125,14 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     S.ykey[i] = (valid && U.active) ? (float)py : __int_as_float(0x7f800000);
     if (i == 0) S.dymax = 0u;
   }
-#ifdef TABX_SELFTEST_RACE  // negative control of the checked build: W > 1 hand-off without its barrier
-  if (W == 1)
-#endif
-  env_sync<W>();
   if (W > 1 && TABX_SWEEP) {
+    // (the ranking's own barrier publishes the positions too)
     rank_by_y<W>(S, i, N);
+#ifndef TABX_SELFTEST_RACE  // negative control of the checked build: the contact
+                            // sweep reads the order without this barrier
+    env_sync<W>();
+#endif
+  } else {
     env_sync<W>();
   }
 
@@ -1126,8 +1184,8 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
       const float yi = S.ykey[i];
       const float lim = sweep_limit(yi, 2.0 * DC->rad_max);
       for (int q = S.rnk[i] + 1; q < N; ++q) {
+        if (!(S.skey[q] - yi <= lim)) break;  // ascending keys (+inf last)
         const int j = S.ord[q];
-        if (!(S.ykey[j] - yi <= lim)) break;  // ascending keys (+inf last)
         const int a = i < j ? i : j, c = i < j ? j : i;
         const double dx = S.px[c] - S.px[a], dy = S.py[c] - S.py[a];
         const double rs = S.rad[a] + S.rad[c];

@@ -69,9 +69,10 @@ def test_parity_cases_through_checked_kernels():
 
 def test_checked_build_catches_a_dropped_barrier():
     """Negative control: the checked build with ONE barrier removed (the
-    W > 1 step kernel's hand-off between publishing the integrated positions
-    and the contact pass, -DTABX_SELFTEST_RACE) must fail the W > 1 parity
-    cases -- evidence that the lane jitter exposes a missing barrier."""
+    W > 1 step kernel's hand-off between ranking the units along y and the
+    contact sweep that reads that order, -DTABX_SELFTEST_RACE, with half the
+    threads publishing their ranks late) must fail the W > 1 parity cases --
+    evidence that the method sees a missing barrier."""
     if not os.path.exists(SELFTEST):
         pytest.fail(f"{SELFTEST} missing: run build() (it builds the negative control too)")
     env = dict(os.environ, TABX_LIB=SELFTEST)
