@@ -107,7 +107,7 @@ struct EnvSmem {
   uint32_t uf[NT];
   uint32_t zin[NT];
   int32_t tgt[NT];
-  uint32_t ball[W];
+  uint32_t ball[8][W];  // env_ballot slots, one per call site (one barrier each)
   // env-wide unit sets as N-bit masks (word k = units 32k..32k+31)
   uint32_t m_active[W], m_alive[W], m_enemy[W], m_rev[W], m_inbush[W];
   uint32_t m_zone[TABX_MAX_ZONES][W];
@@ -128,39 +128,55 @@ __device__ __forceinline__ void env_sync() {
   }
 }
 
-// Env-wide ballot: word k holds predicates of units 32k..32k+31.
-template <int W>
+// Env-wide ballot: word k holds predicates of units 32k..32k+31.  W > 1:
+// every call site has its own slot SL of S.ball, written once per step, so a
+// ballot costs one barrier (a slot is rewritten only in the next step, after
+// that step's opening barrier).
+template <int W, int SL>
 __device__ __forceinline__ void env_ballot(bool p, EnvSmem<W>& S, int i, uint32_t (&m)[W]) {
+  static_assert(SL >= 0 && SL < 8, "ballot slot");
   uint32_t b = __ballot_sync(0xffffffffu, p);
   if (W == 1) {
     m[0] = b;
   } else {
-    if ((i & 31) == 0) S.ball[i >> 5] = b;
+    if ((i & 31) == 0) S.ball[SL][i >> 5] = b;
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < W; ++k) m[k] = S.ball[k];
-    __syncthreads();
+    for (int k = 0; k < W; ++k) m[k] = S.ball[SL][k];
   }
 }
 
-template <int W>
+// Two predicates through slots SL and SL + 1 with one barrier.
+template <int W, int SL>
+__device__ __forceinline__ void env_ballot2(bool p0, bool p1, EnvSmem<W>& S, int i,
+                                            uint32_t (&m0)[W], uint32_t (&m1)[W]) {
+  static_assert(SL >= 0 && SL + 1 < 8, "ballot slot");
+  const uint32_t b0 = __ballot_sync(0xffffffffu, p0), b1 = __ballot_sync(0xffffffffu, p1);
+  if (W == 1) {
+    m0[0] = b0;
+    m1[0] = b1;
+  } else {
+    if ((i & 31) == 0) {
+      S.ball[SL][i >> 5] = b0;
+      S.ball[SL + 1][i >> 5] = b1;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      m0[k] = S.ball[SL][k];
+      m1[k] = S.ball[SL + 1][k];
+    }
+  }
+}
+
+template <int W, int SL>
 __device__ __forceinline__ bool env_any(bool p, EnvSmem<W>& S, int i) {
   uint32_t m[W];
-  env_ballot<W>(p, S, i, m);
+  env_ballot<W, SL>(p, S, i, m);
   uint32_t a = 0;
 #pragma unroll
   for (int k = 0; k < W; ++k) a |= m[k];
   return a != 0;
-}
-
-template <int W>
-__device__ __forceinline__ int env_count(bool p, EnvSmem<W>& S, int i) {
-  uint32_t m[W];
-  env_ballot<W>(p, S, i, m);
-  int c = 0;
-#pragma unroll
-  for (int k = 0; k < W; ++k) c += __popc(m[k]);
-  return c;
 }
 
 // Rank of every unit by its published y key (ties by index), all threads:
@@ -1021,7 +1037,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     S.uf[i] = (U.active ? UF_ACTIVE : 0u) | (alive ? UF_ALIVE : 0u);
     if (W > 1) {
       uint32_t m[W];
-      env_ballot<W>(valid && U.active, S, i, m);
+      env_ballot<W, 0>(valid && U.active, S, i, m);
       if ((i & 31) == 0) S.m_active[i >> 5] = m[i >> 5];
     }
   } else {
@@ -1048,7 +1064,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   if (M == MODE_STEP_K0) {
     // K0 made the decision (its memory update is in the state read above)
     if (heur) act = (int)P.ctrl_act[u];
-  } else if (env_any<W>(heur, S, i)) {
+  } else if (env_any<W, 1>(heur, S, i)) {
     // cached vis/atk of the previous stage 8, or fresh after a batch refill
     if (refresh) {
       cache_row_of<W>(S, i, N, U, bush_m);
@@ -1207,7 +1223,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     bool mine = false;
 #pragma unroll
     for (int k = 0; k < W; ++k) mine |= S.touch[i * W + k] != 0u;
-    env_ballot<W>(mine, S, i, rowm);
+    env_ballot<W, 2>(mine, S, i, rowm);
 #pragma unroll
     for (int k = 0; k < W; ++k) any_touch |= rowm[k] != 0u;
   } else if (TABX_PAIR_CONTACTS) {
@@ -1266,7 +1282,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     bool mine = false;
 #pragma unroll
     for (int k = 0; k < W; ++k) mine |= S.touch[i * W + k] != 0u;
-    env_ballot<W>(mine, S, i, rowm);
+    env_ballot<W, 2>(mine, S, i, rowm);
 #pragma unroll
     for (int k = 0; k < W; ++k) any_touch |= rowm[k] != 0u;
   } else {
@@ -1306,7 +1322,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     }
 #pragma unroll
     for (int k = 0; k < W; ++k) S.touch[i * W + k] = trow[k];
-    env_ballot<W>(mine, S, i, rowm);
+    env_ballot<W, 2>(mine, S, i, rowm);
 #pragma unroll
     for (int k = 0; k < W; ++k) any_touch |= rowm[k] != 0u;
   }
@@ -1425,7 +1441,7 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   env_sync<W>();
   // per-victim damage: landed attackers in ascending order (combat.py:108)
   uint32_t lm[W];
-  env_ballot<W>(landed, S, i, lm);
+  env_ballot<W, 3>(landed, S, i, lm);
   double delta = 0.0;
   bool was_hit = false;
 #pragma unroll
@@ -1453,8 +1469,16 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
   const bool still = alive && hp > 0.0;
   const bool died = alive && !still;
   alive = still;
-  const bool any_died = env_any<W>(died, S, i);
-  const bool ally_died = env_any<W>(died && !U.enemy, S, i);
+  bool any_died = false, ally_died = false;
+  {
+    uint32_t md[W], ma[W];
+    env_ballot2<W, 4>(died, died && !U.enemy, S, i, md, ma);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      any_died |= md[k] != 0u;
+      ally_died |= ma[k] != 0u;
+    }
+  }
   if (any_died && fk < 0) fk = ally_died ? ENEMY : ALLY;
 
   TABX_PHASE(5);
@@ -1467,8 +1491,16 @@ __device__ void run_lane(const Params& P, int64_t b, int i, EnvSmem<W>& S,
     prev_gap = gap;
     t += 1;
   }
-  const int na = env_count<W>(alive && U.active && !U.enemy, S, i);
-  const int ne = env_count<W>(alive && U.active && U.enemy, S, i);
+  int na = 0, ne = 0;
+  {
+    uint32_t mA[W], mE[W];
+    env_ballot2<W, 6>(alive && U.active && !U.enemy, alive && U.active && U.enemy, S, i, mA, mE);
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      na += __popc(mA[k]);
+      ne += __popc(mE[k]);
+    }
+  }
   const bool elim = running && (na == 0 || ne == 0);
   const bool trunc = running && !elim && t >= C->max_steps;
   int win = -1, why = R_NONE;
