@@ -709,14 +709,18 @@ cudaError_t launch_emit_f(const Params& P, int sm_count, cudaStream_t stream) {
 // 6 CTAs without VPF stay faster (C5 43.2 vs 42.4 M env-steps/s).
 template <int NF, int ZF, bool F16>
 struct EmitTune {
-  static constexpr int minb = F16 ? 6 : (NF == 20 && ZF == 6) ? 4 : (NF == 20 && ZF == 0) ? 5 : 6;
+  // resident warps per SM (the register budget follows from it)
+  static constexpr int warps = F16 ? 24 : (NF == 20 && ZF == 6) ? 16 : (NF == 20 && ZF == 0) ? 20 : 24;
   static constexpr bool vpf = !F16 && NF == 20 && ZF == 6;
 };
 
 template <int W, int EPW, bool F16, int NF, int ZF>
 __global__ void __launch_bounds__(32 * EPW,
-                                  (W == 1 ? (TABX_EMIT_MIN_BLOCKS_W1 > 0 ? TABX_EMIT_MIN_BLOCKS_W1
-                                                                         : EmitTune<NF, ZF, F16>::minb)
+                                  (W == 1 ? (TABX_EMIT_MIN_BLOCKS_W1 > 0
+                                                 ? TABX_EMIT_MIN_BLOCKS_W1
+                                                 : (EmitTune<NF, ZF, F16>::warps / EPW > 0
+                                                        ? EmitTune<NF, ZF, F16>::warps / EPW
+                                                        : 1))
                                           : TABX_EMIT_MIN_BLOCKS))
     emit_kernel_fixed(const Params P) {
   constexpr int N = NF, Z = ZF;

@@ -289,7 +289,7 @@ cudaError_t launch_fused_w1(const Params& P, int variant, int sm_count, cudaStre
 namespace tabx {
 
 template <int NF, int ZF, int EPB>
-__global__ void __launch_bounds__(32 * EPB, TABX_MIN_BLOCKS) step_small_kernel(const Params P) {
+__global__ void __launch_bounds__(32 * EPB, TABX_MIN_BLOCKS_W1(EPB)) step_small_kernel(const Params P) {
   constexpr size_t env_bytes = (sizeof(EnvSmem<1>) * EPB + 15) & ~(size_t)15;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   if (P.sync->err_index != NO_ERROR) return;  // an action violated the mask: no mutation

@@ -88,6 +88,11 @@ __device__ __forceinline__ double uniform53(uint64_t seed, uint64_t step, uint64
 #define TABX_SWEEP 1
 #endif
 
+#ifndef TABX_VIS_UNROLL
+#define TABX_VIS_UNROLL 4
+#endif
+constexpr int kVisUnroll = TABX_VIS_UNROLL;  // unroll of the visibility filter loop
+
 // ------------------------------------------------------------- helpers --
 constexpr uint32_t UF_ACTIVE = 1, UF_ALIVE = 2, UF_ENEMY = 4, UF_KIN = 8, UF_INJURED = 16;
 
@@ -488,7 +493,7 @@ __device__ __forceinline__ int cache_row_body(EnvSmem<W>& S, int i, int N, doubl
       q0 = lower_rank<W>(S, N, yi - lim);
       q1 = upper_rank<W>(S, N, yi + lim);
     }
-#pragma unroll 4
+#pragma unroll (kVisUnroll)
     for (int q = q0; q < q1; ++q) {
       const int j = SWEEP ? (int)S.ord[q] : q;
       const float dxf = (float)(S.px[j] - px), dyf = (float)(S.py[j] - py);
@@ -1610,9 +1615,11 @@ __host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
   return emit_warp_bytes<W>(P.N, P.Z, R, SF);
 }
 
-#ifndef TABX_MIN_BLOCKS
-#define TABX_MIN_BLOCKS 4
+#ifndef TABX_K1_EPB
+#define TABX_K1_EPB 16  // W = 1: environments (warps) per step-kernel CTA (4: C3 K1 +10%)
 #endif
+// W = 1: 16 warps/SM at 128 registers whatever the CTA size
+#define TABX_MIN_BLOCKS_W1(EPB) ((16 / (EPB)) > 0 ? (16 / (EPB)) : 1)
 // W > 1 (one env per CTA of 32 W threads): resident warps per SM the
 // register budget is cut for (C4 step kernels: unconstrained 254 registers
 // at 8 warps/SM 11.2 ms; 16 warps at 128 registers 7.8 ms; 24 warps at 80
@@ -1625,7 +1632,7 @@ __host__ __device__ __forceinline__ size_t reset_view_bytes(const Params& P) {
 // One kernel per mode (M): the step kernel carries no reset / emitter code,
 // which keeps its instruction footprint and register allocation to its own.
 template <int W, int EPB, int M, int NF = 0, int ZF = 0>
-__global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS : TABX_MIN_BLOCKS_WN(W)))
+__global__ void __launch_bounds__(32 * W * EPB, (W == 1 ? TABX_MIN_BLOCKS_W1(EPB) : TABX_MIN_BLOCKS_WN(W)))
     lane_kernel(const Params P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   EnvSmem<W>* envs = reinterpret_cast<EnvSmem<W>*>(smem_raw);
@@ -1848,26 +1855,28 @@ cudaError_t launch_lanes_m(const Params& P, int sm_count, cudaStream_t stream, i
   return cudaGetLastError();
 }
 
-template <int W, int EPB>
+// EPB: environments per CTA of the reset / init / refresh kernels; ES: of
+// the step kernels (W = 1)
+template <int W, int EPB, int ES = EPB>
 cudaError_t launch_lanes_t(const Params& P, int sm_count, cudaStream_t stream, int* grid_out) {
   switch (P.mode) {
-    case MODE_STEP: return launch_lanes_m<W, EPB, MODE_STEP>(P, sm_count, stream, grid_out);
+    case MODE_STEP: return launch_lanes_m<W, ES, MODE_STEP>(P, sm_count, stream, grid_out);
     case MODE_STEP_K0:
       // shape-specialised step kernels (C3 / C2 / C1 / C4 shapes); any other
       // shape, or TABX_GENERIC_SHAPES=1, takes the generic one
       if constexpr (W == 1) {
         if (!P.generic_shapes && P.N == 20 && P.Z == 6)
-          return launch_lanes_m<1, EPB, MODE_STEP_K0, 20, 6>(P, sm_count, stream, grid_out);
+          return launch_lanes_m<1, ES, MODE_STEP_K0, 20, 6>(P, sm_count, stream, grid_out);
         if (!P.generic_shapes && P.N == 20 && P.Z == 0)
-          return launch_lanes_m<1, EPB, MODE_STEP_K0, 20, 0>(P, sm_count, stream, grid_out);
+          return launch_lanes_m<1, ES, MODE_STEP_K0, 20, 0>(P, sm_count, stream, grid_out);
         if (!P.generic_shapes && P.N == 6 && P.Z == 0)
-          return launch_lanes_m<1, EPB, MODE_STEP_K0, 6, 0>(P, sm_count, stream, grid_out);
+          return launch_lanes_m<1, ES, MODE_STEP_K0, 6, 0>(P, sm_count, stream, grid_out);
       }
       if constexpr (W == 4) {
         if (!P.generic_shapes && P.N == 100 && P.Z == 0)
-          return launch_lanes_m<4, EPB, MODE_STEP_K0, 100, 0>(P, sm_count, stream, grid_out);
+          return launch_lanes_m<4, ES, MODE_STEP_K0, 100, 0>(P, sm_count, stream, grid_out);
       }
-      return launch_lanes_m<W, EPB, MODE_STEP_K0>(P, sm_count, stream, grid_out);
+      return launch_lanes_m<W, ES, MODE_STEP_K0>(P, sm_count, stream, grid_out);
     case MODE_INIT: return launch_lanes_m<W, EPB, MODE_INIT>(P, sm_count, stream, grid_out);
     case MODE_REFRESH:
       return launch_lanes_m<W, EPB, MODE_REFRESH>(P, sm_count, stream, grid_out);

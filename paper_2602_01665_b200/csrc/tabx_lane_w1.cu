@@ -6,7 +6,7 @@ cudaError_t launch_ctrl_w1(const Params& P, int nh, int sm_count, cudaStream_t s
   return launch_ctrl_t<1>(P, nh, sm_count, stream);
 }
 cudaError_t launch_lanes_w1(const Params& P, int sm_count, cudaStream_t stream, int* grid) {
-  return launch_lanes_t<1, 4>(P, sm_count, stream, grid);
+  return launch_lanes_t<1, 4, TABX_K1_EPB>(P, sm_count, stream, grid);
 }
 // observation-kernel envs (warps) per CTA at W = 1
 #ifndef TABX_EMIT_EPW
