@@ -1718,11 +1718,14 @@ struct CtrlView {
 // K0 resident CTAs per SM the register budget is cut for: W = 1 6 (80
 // registers; 4 and 5 measured neutral at C3), W > 1 4 (128 registers; C4
 // refresh + K0 + K1 7.18 -> 7.05 ms)
+#ifndef TABX_K0_THREADS
+#define TABX_K0_THREADS 128  // threads per K0 CTA
+#endif
 #ifndef TABX_K0_MINB
-#define TABX_K0_MINB(W) ((W) == 1 ? 6 : 4)
+#define TABX_K0_MINB(W) (((W) == 1 ? 768 : 512) / TABX_K0_THREADS)
 #endif
 template <int W>
-__global__ void __launch_bounds__(128, TABX_K0_MINB(W)) ctrl_kernel(const Params P, int G, int NH) {
+__global__ void __launch_bounds__(TABX_K0_THREADS, TABX_K0_MINB(W)) ctrl_kernel(const Params P, int G, int NH) {
   if (P.sync->err_index != NO_ERROR) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1823,7 +1826,7 @@ cudaError_t launch_ctrl_t(const Params& P, int nh, int sm_count, cudaStream_t st
   if (G > 8) G = 8;
   if (W > 1) G = 1;
   const int NH = nh < 32 ? nh : 32;
-  const int threads = 128;
+  const int threads = TABX_K0_THREADS;
   const size_t smem = sizeof(CtrlView<W>) * G * (threads / 32);
   int per_sm = 1;
   cudaError_t e = launch_geometry((const void*)ctrl_kernel<W>, threads, smem, &per_sm);
