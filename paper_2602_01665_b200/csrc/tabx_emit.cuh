@@ -63,68 +63,6 @@ __device__ __forceinline__ bool row_bit(const uint32_t* row, int j) {
   return (row[j >> 5] >> (j & 31)) & 1u;
 }
 
-// L2 prefetch of a byte range (TMA, one instruction, no registers held):
-// the rounded-out 16-byte-aligned cover of [p, p + bytes).
-__device__ __forceinline__ void l2_prefetch(const void* p, size_t bytes) {
-  const uintptr_t a = (uintptr_t)p & ~(uintptr_t)15;
-  const uintptr_t e = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a), "r"((uint32_t)(e - a))
-               : "memory");
-}
-
-#ifndef TABX_EMIT_PREFETCH
-#define TABX_EMIT_PREFETCH 0  // 1: TMA L2 prefetch one env ahead (10% slower), 2: LSU line prefetch one env ahead (2% slower), 3: LSU prefetch two chunks ahead (4% slower)
-#endif
-// (2: per-lane LSU line prefetches one env ahead)
-
-// Per-lane L2 line prefetches (LSU, no TMA, no registers held) of env b's
-// per-unit state arrays the view reads: lane = 4 * array + 128-byte piece.
-template <int W>
-__device__ __forceinline__ void prefetch_env_lines(const DevState& st, int64_t b, int N,
-                                                   int lane) {
-  const int64_t u = b * N;
-  const int a = lane >> 2, piece = lane & 3;
-  const char* base = nullptr;
-  size_t bytes = 0;
-  switch (a) {
-    case 0: base = (const char*)(st.pos + u); bytes = (size_t)16 * N; break;
-    case 1: base = (const char*)(st.hcs + u); bytes = (size_t)16 * N; break;
-    case 2: base = (const char*)(st.health + u); bytes = (size_t)8 * N; break;
-    case 3: base = (const char*)(st.cooldown + u); bytes = (size_t)8 * N; break;
-    case 4: base = (const char*)(st.ubits + u); bytes = (size_t)N; break;
-    case 5: base = (const char*)(st.vis + u * W); bytes = (size_t)4 * W * N; break;
-    case 6: base = (const char*)(st.atk + u * W); bytes = (size_t)4 * W * N; break;
-    default: break;
-  }
-  // the 128-byte lines covering [base, base + bytes): piece k = line k
-  const uintptr_t l0 = (uintptr_t)base & ~(uintptr_t)127;
-  const uintptr_t p = l0 + (uintptr_t)piece * 128;
-  if (base && p < (uintptr_t)base + bytes)
-    asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p));
-}
-
-// Lanes 0..6 each pull one of env b's per-unit state arrays the view reads
-// into L2 (the emit loop issues this one env ahead).
-template <int W>
-__device__ __forceinline__ void prefetch_env_state(const DevState& st, int64_t b, int N,
-                                                   int lane) {
-  if (TABX_EMIT_PREFETCH == 2) {
-    prefetch_env_lines<W>(st, b, N, lane);
-    return;
-  }
-  const int64_t u = b * N;
-  switch (lane) {
-    case 0: l2_prefetch(st.pos + u, (size_t)16 * N); break;
-    case 1: l2_prefetch(st.hcs + u, (size_t)16 * N); break;
-    case 2: l2_prefetch(st.health + u, (size_t)8 * N); break;
-    case 3: l2_prefetch(st.cooldown + u, (size_t)8 * N); break;
-    case 4: l2_prefetch(st.ubits + u, (size_t)N); break;
-    case 5: l2_prefetch(st.vis + u * W, (size_t)4 * W * N); break;
-    case 6: l2_prefetch(st.atk + u * W, (size_t)4 * W * N); break;
-    default: break;
-  }
-}
-
 // Own-feature block of unit u from its state values (perception.py:108-132).
 __device__ __forceinline__ void own_from_vals(float* o, double2 p, double2 cs, double hp,
                                               double cd, uint8_t ub,
@@ -379,8 +317,7 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
                           float* __restrict__ glob, int64_t b, int N, int Z, int D, int G, int R,
                           int SF, const tabx_config* __restrict__ C,
                           const DerivedCfg* __restrict__ DC, int lane, int& buf, bool drain,
-                          __nv_bfloat16* __restrict__ o16 = nullptr, int ld16 = 0,
-                          const DevState* pf_st = nullptr, int64_t pf_b = -1) {
+                          __nv_bfloat16* __restrict__ o16 = nullptr, int ld16 = 0) {
   const EmitEnv<W>& E = X.E;
   const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
   const int M = N - 1;
@@ -412,11 +349,6 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
     for (int r0 = 0; r0 < N; r0 += R) {
       const int nr = min(R, N - r0);
       const int64_t gs = (b * N + r0) * (int64_t)D;
-#if TABX_EMIT_PREFETCH == 3
-      // the next env's view lines into L2 two chunks before this env ends
-      // (a longer distance loses them to the row stream's L2 turnover)
-      if (pf_b >= 0 && r0 + 2 * R >= N && r0 + R < N) prefetch_env_lines<W>(*pf_st, pf_b, N, lane);
-#endif
       TABX_ASSERT(nr > 0 && (pad_fits(gs, nr * D, SF)));
       TABX_JITTER(301);
       float* st = X.stage + buf * SF;
@@ -742,9 +674,6 @@ __global__ void __launch_bounds__(32 * EPW,
   // does not start with a dependent chain of DRAM round trips
   int32_t k_next = b < P.B ? st.cfg[b] : 0;
   uint8_t f_next = b < P.B ? st.flags[b] : 0;
-#if TABX_EMIT_PREFETCH && TABX_EMIT_PREFETCH != 3
-  if (b < P.B) prefetch_env_state<W>(st, b, N, lane);
-#endif
   // (W = 1, TABX_EMIT_VIEW_PREFETCH) the next env's view inputs are loaded
   // into registers before this env's rows stream out
   constexpr bool VPF =
@@ -758,9 +687,6 @@ __global__ void __launch_bounds__(32 * EPW,
     if (b + stride < P.B) {
       k_next = st.cfg[b + stride];
       f_next = st.flags[b + stride];
-#if TABX_EMIT_PREFETCH && TABX_EMIT_PREFETCH != 3
-      prefetch_env_state<W>(st, b + stride, N, lane);
-#endif
       if (VPF) fetch_view_regs(V_next, st, b + stride, N, lane);
     }
     const tabx_config* C = P.cfgs + k;
@@ -775,7 +701,7 @@ __global__ void __launch_bounds__(32 * EPW,
     else
       load_view<W>(X, st, b, N, Z, C, DC, lane);
     emit_lane<W, F16>(X, ob, gb, b, N, Z, D, G, R, SF, C, DC, lane, buf, false, o16,
-                      (int)P.out.observations_bf16_ld, &st, b + stride < P.B ? b + stride : -1);
+                      (int)P.out.observations_bf16_ld);
   }
   if (lane == 0) bulk_wait_all();
 }
