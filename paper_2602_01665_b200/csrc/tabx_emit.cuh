@@ -317,7 +317,8 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
                           float* __restrict__ glob, int64_t b, int N, int Z, int D, int G, int R,
                           int SF, const tabx_config* __restrict__ C,
                           const DerivedCfg* __restrict__ DC, int lane, int& buf, bool drain,
-                          __nv_bfloat16* __restrict__ o16 = nullptr, int ld16 = 0) {
+                          __nv_bfloat16* __restrict__ o16 = nullptr, int ld16 = 0,
+                          int rbeg = 0, int rstep = 1) {
   const EmitEnv<W>& E = X.E;
   const double fw = C->field_w, fh = C->field_h, rw = DC->rw, rh = DC->rh;
   const int M = N - 1;
@@ -346,7 +347,9 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
   const double rel_f = rel_ax ? fh : fw, rel_rf = rel_ax ? rh : rw;
   const int rel_off = rel_rr * D + zoff + rel_z * TABX_ZONE_DIM + 3 + rel_ax;
   if (obs || (F16 && o16)) {
-    for (int r0 = 0; r0 < N; r0 += R) {
+    // (rbeg, rstep: this warp's share of the chunks when several warps
+    // emit one environment, emit_kernel_cta)
+    for (int r0 = rbeg * R; r0 < N; r0 += rstep * R) {
       const int nr = min(R, N - r0);
       const int64_t gs = (b * N + r0) * (int64_t)D;
       TABX_ASSERT(nr > 0 && (pad_fits(gs, nr * D, SF)));
@@ -741,8 +744,106 @@ cudaError_t launch_emit_shape(const Params& P, int sm_count, cudaStream_t stream
   return launch_emit_f<W, EPW, F16>(P, sm_count, stream);
 }
 
+// W > 1: one environment per CTA of WPE warps.  The CTA loads the env's
+// view once into shared memory (N units over 32 WPE threads) and the warps
+// split its row chunks (warp w: chunks w, w + WPE, ...; warp 0 also the
+// global-state row), each through its own double-buffered TMA stage.  The
+// one-warp-per-env emitter holds a whole view (13 KB at N = 100) plus two
+// 6.8 KB stages per warp, which capped it at 8 warps/SM; sharing the view
+// fits 12.
+template <int W, int WPE, bool F16, int NF, int ZF>
+__global__ void __launch_bounds__(32 * WPE) emit_kernel_cta(const Params P, int R, int SF) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (is_step_mode(P.mode) && P.sync->err_index != NO_ERROR) return;
+  const int N = NF ? NF : P.N, Z = NF ? ZF : P.Z;
+  const int D = NF ? TABX_OWN_DIM + TABX_OTHER_DIM * (NF - 1) + TABX_ZONE_DIM * ZF : P.D;
+  const int G = NF ? TABX_OWN_DIM * NF + TABX_ZONE_DIM * ZF : P.G;
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const size_t vb = emit_view_bytes<W>(N);
+  EmitScratch<W> X = emit_scratch<W>(smem_raw, N, Z, R);
+  X.stage = reinterpret_cast<float*>(smem_raw + vb) + (size_t)w * TABX_EMIT_NBUF * SF;
+  const EmitEnv<W>& E = X.E;
+  const DevState& st = P.st;
+  int buf = 0;
+  for (int64_t b = blockIdx.x; b < P.B; b += gridDim.x) {
+    const int32_t k = st.cfg[b];
+    const tabx_config* C = P.cfgs + k;
+    const DerivedCfg* DC = P.dcfgs + k;
+    const bool pending = (st.flags[b] & F_PEND) != 0;
+    float* ob = pending ? P.out.final_observations : P.out.observations;
+    float* gb = pending ? P.out.final_global_state : P.out.global_state;
+    __nv_bfloat16* o16 = (F16 && !pending) ? (__nv_bfloat16*)P.out.observations_bf16 : nullptr;
+    if (!ob && !gb && !o16) continue;  // CTA-uniform
+    __syncthreads();  // every warp is done with the previous env's view
+    TABX_POISON(X.E.px, vb, tid, 32 * WPE);
+    __syncthreads();
+    for (int u = tid; u < N; u += 32 * WPE) {
+      const int64_t gu = b * N + u;
+      const double2 p = st.pos[gu];
+      E.px[u] = p.x;
+      E.py[u] = p.y;
+      own_from_state(E.own[u], st, gu, C, DC, u);
+      E.flags[u] = (C->active[u] ? 1u : 0u) | (C->team[u] ? 2u : 0u);
+#pragma unroll
+      for (int kk = 0; kk < W; ++kk) {
+        E.vis[u * W + kk] = st.vis[gu * W + kk];
+        E.atk[u * W + kk] = st.atk[gu * W + kk];
+      }
+    }
+    __syncthreads();
+    emit_lane<W, F16>(X, ob, w == 0 ? gb : nullptr, b, N, Z, D, G, R, SF, C, DC, lane, buf, false,
+                      o16, (int)P.out.observations_bf16_ld, w, WPE);
+  }
+  if (lane == 0) bulk_wait_all();
+}
+
+// W > 1: warps per environment of the observation kernel (0: the one-warp
+// emitter).  Measured (tools/wprobe.py, kab): W = 2 (40 units) 1.96 -> 1.62 ms
+// with 2 (4: 2.03); W = 4 (C4, 100 units) neutral with 4, +0.7% with 2: kept
+// at one; W = 8 (150 units) 6.91 -> 5.97 ms with 2, 4.88 ms with 4.
+#ifndef TABX_EMIT_WPE_W2
+#define TABX_EMIT_WPE_W2 2
+#endif
+#ifndef TABX_EMIT_WPE_W4
+#define TABX_EMIT_WPE_W4 0
+#endif
+#ifndef TABX_EMIT_WPE_W8
+#define TABX_EMIT_WPE_W8 4
+#endif
+template <int W>
+constexpr int emit_wpe() {
+  return W == 2 ? TABX_EMIT_WPE_W2 : W == 4 ? TABX_EMIT_WPE_W4 : W == 8 ? TABX_EMIT_WPE_W8 : 0;
+}
+
+template <int W, bool F16, int NF, int ZF>
+cudaError_t launch_emit_cta(const Params& P, int sm_count, cudaStream_t stream) {
+  constexpr int WPE = emit_wpe<W>() > 0 ? emit_wpe<W>() : 1;
+  const int R = emit_rows(P.N, P.D, 8192);
+  const int SF = emit_stage_floats(P.N, P.D, P.G, R);
+  const size_t smem = emit_view_bytes<W>(P.N) + (size_t)WPE * TABX_EMIT_NBUF * SF * sizeof(float);
+  int per_sm = 0;
+  auto kern = emit_kernel_cta<W, WPE, F16, NF, ZF>;
+  cudaError_t e = launch_geometry((const void*)kern, 32 * WPE, smem, &per_sm);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorNotSupported;
+  const int64_t cap = (int64_t)sm_count * per_sm;
+  int grid = (int)(P.B < cap ? P.B : cap);
+  if (grid < 1) grid = 1;
+  kern<<<grid, 32 * WPE, smem, stream>>>(P, R, SF);
+  return cudaGetLastError();
+}
+
 template <int W, int EPW>
 cudaError_t launch_emit_t(const Params& P, int sm_count, cudaStream_t stream) {
+  if constexpr (W > 1 && emit_wpe<W>() > 0) {
+    if constexpr (W == 4) {
+      if (!P.generic_shapes && P.N == 100 && P.Z == 0)
+        return P.out.observations_bf16 ? launch_emit_cta<4, true, 100, 0>(P, sm_count, stream)
+                                       : launch_emit_cta<4, false, 100, 0>(P, sm_count, stream);
+    }
+    return P.out.observations_bf16 ? launch_emit_cta<W, true, 0, 0>(P, sm_count, stream)
+                                   : launch_emit_cta<W, false, 0, 0>(P, sm_count, stream);
+  }
   return P.out.observations_bf16 ? launch_emit_shape<W, EPW, true>(P, sm_count, stream)
                                  : launch_emit_shape<W, EPW, false>(P, sm_count, stream);
 }
