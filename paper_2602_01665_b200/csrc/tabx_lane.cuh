@@ -624,9 +624,11 @@ __device__ __forceinline__ void team_ratios(EnvSmem<W>& S, int i, int N, bool ac
   env_sync<W>();
   const double ca = (double)(n_ally > 1 ? n_ally : 1);
   const double ce = (double)(n_enemy > 1 ? n_enemy : 1);
-  if (W == 1 && N >= 8) {
-    // numpy's 8-accumulator block (n <= 128): lanes 0-7 / 8-15 run the ally /
-    // enemy accumulators, lanes 0 and 8 combine them in numpy's tree order
+  if (N >= 8 && N <= 128) {
+    // numpy's 8-accumulator block (n <= 128): threads 0-7 / 8-15 run the ally /
+    // enemy accumulators, threads 0 and 8 combine them in numpy's tree order
+    // (W > 1 too: one thread summing 2 x 100 values serially held the other
+    // warps at the next barrier)
     const int lim = N - (N % 8);
     if (i < 16) {
       const double* v = i < 8 ? S.vx : S.vy;
