@@ -101,8 +101,7 @@ struct EnvSmem {
   // the units in ascending key order and each unit's rank in it
   float ykey[NT], skey[NT];  // skey[r] = key of the unit of rank r
   int16_t ord[NT], rnk[NT];
-  float rk_key[NT];  // per-warp sorted runs (rank_by_y)
-  int16_t rk_id[NT];
+  unsigned long long rk_key[NT];  // per-warp sorted runs of (key bits, index) (rank_by_y)
   uint32_t dymax;  // float bits: largest |y| move since the keys were taken
   uint32_t uf[NT];
   uint32_t zin[NT];
@@ -188,38 +187,34 @@ template <int W>
 __device__ __forceinline__ void rank_by_y(EnvSmem<W>& S, int i, int N) {
   const uint32_t full = 0xffffffffu;
   const int lane = i & 31, w = i >> 5;
-  float k = S.ykey[i];  // +inf for inactive units and threads past N
-  int id = i;
+  const float f = S.ykey[i];  // +inf for inactive units and threads past N
+  // one 64-bit key, unique per unit: the float's order-preserving bits, then
+  // the index (ties by index)
+  const uint32_t fb = __float_as_uint(f);
+  const uint32_t ob = (fb & 0x80000000u) ? ~fb : (fb | 0x80000000u);
+  unsigned long long key = ((unsigned long long)ob << 32) | (unsigned)i;
 #pragma unroll
   for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const float ok = __shfl_xor_sync(full, k, stride);
-      const int oid = __shfl_xor_sync(full, id, stride);
+      const unsigned long long ok = __shfl_xor_sync(full, key, stride);
       const bool up = (lane & size) == 0;
       const bool lower = (lane & stride) == 0;
-      const bool o_less = (ok < k) || (ok == k && oid < id);
-      const bool take = lower ? (up ? o_less : !o_less) : (up ? !o_less : o_less);
-      if (take) {
-        k = ok;
-        id = oid;
-      }
+      // the lower position keeps the smaller key in an ascending block
+      if ((ok < key) == (lower == up)) key = ok;
     }
   }
-  S.rk_key[i] = k;
-  S.rk_id[i] = (int16_t)id;
+  S.rk_key[i] = key;
   env_sync<W>();
   int r = lane;
 #pragma unroll
   for (int w2 = 0; w2 < W; ++w2) {
     if (w2 == w) continue;
-    const float* rk = S.rk_key + w2 * 32;
-    const int16_t* ri = S.rk_id + w2 * 32;
+    const unsigned long long* rk = S.rk_key + w2 * 32;
     int lo = 0, hi = 32;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      const float kk = rk[mid];
-      if (kk < k || (kk == k && ri[mid] < id)) lo = mid + 1; else hi = mid;
+      if (rk[mid] < key) lo = mid + 1; else hi = mid;
     }
     r += lo;
   }
@@ -227,10 +222,11 @@ __device__ __forceinline__ void rank_by_y(EnvSmem<W>& S, int i, int N) {
   // negative control: half the threads publish their ranks 20 us late
   if ((threadIdx.x * 0x9E3779B9u) >> 31) __nanosleep(20000);
 #endif
+  const int id = (int)(key & 0xffffffffu);
   if (id < N) {
     S.ord[r] = (int16_t)id;
     S.rnk[id] = (int16_t)r;
-    S.skey[r] = k;
+    S.skey[r] = S.ykey[id];
   }
 }
 
