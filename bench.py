@@ -356,6 +356,23 @@ def roofline(key: str, N: int, Z: int, per: int, kern_ms: float, kprof: dict) ->
             strict = (4 * N * D + 4 * G) * per / (ms / 1000.0) / 1e9
             ent["frac_obs_bytes_only"] = strict / peak
         kernels.append(ent)
+    # issue roofline of the latency-bound step kernels: ncu warp-instruction
+    # counts per env-step (profiles/instructions_<key>.json) over the measured
+    # time, against 4 warp-instructions per SM-cycle at the max SM clock
+    ins = os.path.join(ROOT, "profiles", f"instructions_{key}.json")
+    if os.path.exists(ins):
+        with open(ins) as fh:
+            doc = json.load(fh)
+        wi = doc["warp_instructions"]
+        mhz = peaks.get("sm_max_mhz", 1965.0)
+        peak_ips = doc["peak_warp_instructions_per_sm_cycle"] * doc["sm_count"] * mhz * 1e6
+        for ent in kernels:
+            parts = (("K0", "K1") if ent["kernel"].startswith("step_kernels") else
+                     ("K2",) if ent["kernel"].startswith("obs_kernel") else ())
+            if parts and ent.get("ms_avg"):
+                n = sum(wi[p] for p in parts) / doc["envs"] * per
+                ent["warp_instructions_per_env_step"] = round(n / per, 1)
+                ent["issue_frac"] = n / (ent["ms_avg"] / 1000.0) / peak_ips
     traffic = None
     prof = os.path.join(ROOT, "profiles", f"traffic_{key}.json")
     if os.path.exists(prof):
