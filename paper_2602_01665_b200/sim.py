@@ -246,16 +246,20 @@ class BatchSim:
             cur.wait_stream(self._stream)
 
     # ---------------------------------------------------------------- api --
-    def step(self, actions=None, strict: bool | None = None) -> BatchOutput:
+    def step(self, actions=None, strict: bool | None = None, outs=None) -> BatchOutput:
         """One step of every lane; ``strict`` (default: the simulator's)
-        raises a latched ActionMaskError synchronously."""
+        raises a latched ActionMaskError synchronously.  ``outs`` (a
+        ``TabxOutputs`` by reference) redirects outputs away from the
+        simulator's own buffers (``HostStepper`` writes each step's rewards /
+        flags straight into its per-slot buffers; the returned view then holds
+        stale values for those fields)."""
         act_t = None
         if actions is not None:
             act_t = self._actions_tensor(actions)
         if self._side_stream:
             self._consume(act_t)
         # (the C side selects the handle's device for its launches)
-        rc = self._step_fn(self._h, _ptr(act_t), self._outs_ref)
+        rc = self._step_fn(self._h, _ptr(act_t), self._outs_ref if outs is None else outs)
         if rc:
             nat.check(rc, "tabx_step")
         self._keep_actions = act_t  # keep alive until the stream consumed it
