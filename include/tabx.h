@@ -336,6 +336,31 @@ int tabx_get_profile(tabx_handle* h, double* ms, int64_t* steps);
 int tabx_step_path(const tabx_handle* h, int32_t* fused);
 
 /*
+ * Native pipelined host stepping (the trainer's host-array loop; the Python
+ * bindings.HostStepper drives it).  tabx_pipe_create keeps `depth` (<=
+ * TABX_PIPE_MAX_DEPTH) slots of device / pinned host buffers; `base` is the
+ * handle's outputs (observations, masks, ... stay where they point; each
+ * step's rewards / terminated / truncated go to the slot's own buffers);
+ * `stream` is the handle's stream.  tabx_pipe_submit copies host int64
+ * actions [B*N] (pinned memory for an asynchronous copy) to the device on an
+ * upload stream, runs tabx_step, and downloads the slot's results on a
+ * download stream, returning a ticket; it first waits until the results of
+ * the step `depth` tickets earlier reached the host.  tabx_pipe_result
+ * waits for ticket's results and returns pointers to them in pinned host
+ * memory (valid until the slot is reused) and the latched action-error
+ * index (-1: none; the caller clears the latch with tabx_get_error).
+ */
+#define TABX_PIPE_MAX_DEPTH 4
+typedef struct tabx_pipe tabx_pipe;
+int tabx_pipe_create(tabx_handle* h, int32_t depth, const tabx_outputs* base, void* stream,
+                     tabx_pipe** out);
+int tabx_pipe_submit(tabx_pipe* p, const int64_t* host_actions, int64_t* ticket);
+int tabx_pipe_result(tabx_pipe* p, int64_t ticket, const float** rewards,
+                     const uint8_t** terminated, const uint8_t** truncated,
+                     int64_t* error_index);
+int tabx_pipe_destroy(tabx_pipe* p);
+
+/*
  * Config table management.  The table starts with the configs given to
  * tabx_create (plus those added by tabx_reset_env); tabx_reserve_configs
  * grows its capacity (synchronises; reallocates the table, so CUDA graphs

@@ -139,6 +139,10 @@ def lib() -> ct.CDLL:
         "tabx_set_profiling": (_i32, [P, _i32]),
         "tabx_get_profile": (_i32, [P, P, P]),
         "tabx_step_path": (_i32, [P, P]),
+        "tabx_pipe_create": (_i32, [P, _i32, P, P, P]),
+        "tabx_pipe_submit": (_i32, [P, P, P]),
+        "tabx_pipe_result": (_i32, [P, ct.c_int64, P, P, P, P]),
+        "tabx_pipe_destroy": (_i32, [P]),
         "tabx_debug_sincos": (_i32, [P, P, P, _i64, P]),
         "tabx_pack_bf16": (_i32, [P, _i64, _i32, _i32, P, P]),
         "tabx_masked_sample": (_i32, [P, _i32, _i64, P, _i64, ct.c_uint64, P, ct.c_uint64, P, P,
