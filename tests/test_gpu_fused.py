@@ -135,12 +135,13 @@ def test_single_launch_step_equals_split(scen, B, steps, monkeypatch):
         assert resets > 0  # auto-resets happened inside the single kernel
 
 
-def test_single_launch_step_matches_oracle(monkeypatch):
-    """C1 (the BASELINE parity config, 256 envs) through the single-launch step
-    against the oracle for 120 steps, auto-resets included."""
+@pytest.mark.parametrize("B", [1, 5, 256])
+def test_single_launch_step_matches_oracle(B, monkeypatch):
+    """C1 (the BASELINE parity config, 256 envs; and ragged 1 / 5 envs: one
+    CTA with idle warps) through the single-launch step against the oracle
+    for 120 steps, auto-resets included."""
     monkeypatch.setenv("TABX_NO_K0", "1")
     sc = builtin_scenario("c1_3v3").scripted()
-    B = 256
     seeds = np.arange(B, dtype=np.uint64) + 900
     gpu = BatchSim([sc] * B, seeds, auto_reset=True, device="cuda:0")
     ora = orc.OracleBatchSim([sc] * B, seeds, auto_reset=True)
