@@ -212,6 +212,11 @@ __device__ __forceinline__ void load_view_regs(const EmitScratch<1>& X, const Vi
 #define TABX_EMIT_VIEW_PREFETCH -1  // -1: per shape (EmitTune), 0 / 1: off / on
 #endif
 
+// bf16 policy-feed stores with the streaming cache hint (st.global.cs)
+#ifndef TABX_EMIT_F16_STCS
+#define TABX_EMIT_F16_STCS 1  // C5 +1% (4 paired runs)
+#endif
+
 // stage buffers per warp (2: fill one while the bulk store drains the other)
 #ifndef TABX_EMIT_NBUF
 #define TABX_EMIT_NBUF 2
@@ -489,7 +494,11 @@ __device__ void emit_lane(const EmitScratch<W>& X, float* __restrict__ obs,
                 v[k] = __floats2bfloat162_rn(c0 + 2 * k < D ? src[c0 + 2 * k] : 0.0f,
                                              c0 + 2 * k + 1 < D ? src[c0 + 2 * k + 1] : 0.0f);
             }
+#if TABX_EMIT_F16_STCS
+            __stcs(reinterpret_cast<uint4*>(dst + c0), *reinterpret_cast<const uint4*>(v));
+#else
             *reinterpret_cast<uint4*>(dst + c0) = *reinterpret_cast<const uint4*>(v);
+#endif
           }
         }
       }
