@@ -57,6 +57,32 @@ def test_dims_and_errors_without_gpu(lib):
     assert b"bad argument" in lib.tabx_last_error()
 
 
+@pytest.mark.parametrize("n,z", [(257, 0), (20, 33), (0, 0)])
+def test_capacity_limits_fail_loudly(lib, n, z):
+    """The documented capacity (N <= 256 units, Z <= 32 zones)
+    is a loud error at both layers, never a silent truncation: the host
+    template raises ValueError and tabx_create returns TABX_E_ARGUMENT
+    before touching the device."""
+    import numpy as np
+
+    from paper_2602_01665_b200 import _native as nat
+    from paper_2602_01665_b200.scenario import builtin_scenario
+    from paper_2602_01665_b200.template import build_config
+
+    sc = builtin_scenario("c3_10v10_terrain")
+    sc.max_units, sc.max_zones = n, z
+    with pytest.raises(ValueError, match="outside"):
+        build_config(sc, validate=False)
+    cfg = build_config(builtin_scenario("c3_10v10_terrain"))
+    cfg.n_units, cfg.n_zones = n, z
+    seeds = np.zeros(1, dtype=np.uint64)
+    h = ct.c_void_p()
+    rc = lib.tabx_create(ct.byref(cfg), 1, None, seeds.ctypes.data, 1, 1, 0, None, ct.byref(h))
+    assert rc == 1 and not h.value
+    assert b"capacity out of range" in lib.tabx_last_error()
+    assert nat.MAX_UNITS == 256 and nat.MAX_ZONES == 32
+
+
 def test_template_matches_oracle_spawn():
     """Host template values equal the oracle's fill_env columns (bit-exact)."""
     import numpy as np
