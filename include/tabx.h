@@ -422,6 +422,18 @@ int tabx_pack_bf16(const float* src, int64_t rows, int32_t d, int32_t dp, void* 
                    void* stream);
 
 /*
+ * Policy MLP of the rollout loop (C5) on the tcgen05 tensor cores, one pass
+ * over the input: logits[r] = W2 · bf16(relu(W1 · x[r] + b1)) + b2 for rows
+ * r < rows.  x: bfloat16 [rows, ldx] (first k features used; k and ldx
+ * multiples of 8, 16-byte aligned), W1 bfloat16 [128, k], b1 [128], W2
+ * bfloat16 [8, 128], b2 [8] (torch Linear layouts), logits bfloat16
+ * [rows, 8], 16-byte aligned.  fp32 accumulation; the hidden activations are
+ * rounded to bfloat16 like the torch module's.  Asynchronous on `stream`.
+ */
+int tabx_policy_mlp(const void* x, int64_t rows, int32_t k, int64_t ldx, const void* w1,
+                    const void* b1, const void* w2, const void* b2, void* logits, void* stream);
+
+/*
  * Tool hook: SM cycles per step phase summed over envs (all step kernels),
  * nonzero only in a build with -DTABX_PHASE_PROF (tools/phase_prof.py).
  */

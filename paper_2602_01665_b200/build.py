@@ -23,7 +23,7 @@ OUT = os.environ.get("TABX_BUILD_OUT") or os.path.join(HERE, "_tabx.so")
 BUILD = os.path.join(ROOT, "build", "tabx")
 
 UNITS = ["tabx_lane_w1.cu", "tabx_lane_w2.cu", "tabx_lane_w4.cu", "tabx_lane_w8.cu",
-         "tabx_fused.cu", "tabx_aux.cu", "tabx_levels.cu", "tabx_policy.cu", "tabx_pipe.cu", "tabx_capi.cu"]
+         "tabx_fused.cu", "tabx_aux.cu", "tabx_levels.cu", "tabx_policy.cu", "tabx_mlp.cu", "tabx_pipe.cu", "tabx_capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 EXTRA = os.environ.get("TABX_NVCC_EXTRA", "").split()
 FLAGS = EXTRA + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",

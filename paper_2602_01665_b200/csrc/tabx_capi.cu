@@ -19,6 +19,9 @@ cudaError_t launch_ctrl(const Params& P, int W, int nh, int sm_count, cudaStream
 cudaError_t launch_emit(const Params& P, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_fused_w1(const Params& P, int variant, int sm_count, cudaStream_t stream);
 cudaError_t launch_small_w1(const Params& P, int sm_count, cudaStream_t stream);
+cudaError_t launch_mlp_policy(const void* x, int64_t rows, int K, int64_t ldx, const void* w1,
+                              const void* b1, const void* w2, const void* b2, void* out,
+                              int sm_count, cudaStream_t stream);
 cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
                             int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream);
 cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const DerivedCfg* dcfgs,
@@ -959,6 +962,20 @@ int tabx_pack_bf16(const float* src, int64_t rows, int32_t d, int32_t dp, void* 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   TABX_CUDA(launch_pack_bf16(src, rows, d, dp, dst, sms, (cudaStream_t)stream), "pack bf16");
+  return TABX_OK;
+}
+
+int tabx_policy_mlp(const void* x, int64_t rows, int32_t k, int64_t ldx, const void* w1,
+                    const void* b1, const void* w2, const void* b2, void* logits, void* stream) {
+  if (rows < 0 || k < 8 || (k & 7) || ldx < k || (ldx & 7) ||
+      (rows > 0 && (!x || !w1 || !b1 || !w2 || !b2 || !logits)) ||
+      (((uintptr_t)x | (uintptr_t)w1 | (uintptr_t)logits) & 15))
+    return fail(TABX_E_ARGUMENT, "tabx_policy_mlp: bad argument");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  TABX_CUDA(launch_mlp_policy(x, rows, k, ldx, w1, b1, w2, b2, logits, sms, (cudaStream_t)stream),
+            "policy mlp");
   return TABX_OK;
 }
 
