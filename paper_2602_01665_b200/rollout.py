@@ -31,7 +31,12 @@ from .sim import BatchSim
 
 
 class MLPPolicy(torch.nn.Module):
-    """Two-layer MLP over padded per-agent observations -> 8 logits (7 used)."""
+    """Two-layer MLP over padded per-agent observations -> 8 logits (7 used).
+
+    On CUDA (bf16, hidden 128) the forward is one launch of the library's
+    tcgen05 kernel (``tabx_policy_mlp``: x read once, the hidden tile kept in
+    TMEM / registers, fp32 accumulation, hidden rounded to bf16);
+    ``reference`` is the same function in torch ops (tests and CPU)."""
 
     def __init__(self, obs_dim: int, hidden: int = 128, n_actions: int = 7):
         super().__init__()
@@ -39,13 +44,29 @@ class MLPPolicy(torch.nn.Module):
         self.l1 = torch.nn.Linear(self.in_dim, hidden)
         self.l2 = torch.nn.Linear(hidden, (n_actions + 7) // 8 * 8)
 
-    def forward(self, obs: torch.Tensor) -> torch.Tensor:
+    def reference(self, obs: torch.Tensor) -> torch.Tensor:
         x = obs.reshape(-1, self.in_dim)
-        # bias + ReLU in the first GEMM's epilogue (cuBLASLt), no separate
-        # pass over the hidden activations
+        # bias + ReLU in the first GEMM's epilogue (cuBLASLt on CUDA)
         h = torch._addmm_activation(self.l1.bias, x, self.l1.weight.t())
         out = torch.addmm(self.l2.bias, h, self.l2.weight.t())
         return out.reshape(*obs.shape[:-1], out.shape[-1])
+
+    def forward(self, obs: torch.Tensor) -> torch.Tensor:
+        if not obs.is_cuda:
+            return self.reference(obs)
+        if (self.l1.out_features != 128 or self.l2.out_features != 8
+                or obs.dtype != torch.bfloat16 or self.l1.weight.dtype != torch.bfloat16):
+            raise ValueError("tabx_policy_mlp needs bf16, hidden 128, 8 logits")
+        x = obs.reshape(-1, self.in_dim)
+        if x.stride(-1) != 1:
+            x = x.contiguous()
+        out = torch.empty(x.shape[0], 8, device=x.device, dtype=torch.bfloat16)
+        ptr = lambda t: ct.c_void_p(t.data_ptr())  # noqa: E731
+        nat.check(nat.lib().tabx_policy_mlp(
+            ptr(x), x.shape[0], self.in_dim, x.stride(0), ptr(self.l1.weight), ptr(self.l1.bias),
+            ptr(self.l2.weight), ptr(self.l2.bias), ptr(out),
+            ct.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)), "tabx_policy_mlp")
+        return out.reshape(*obs.shape[:-1], 8)
 
 
 def masked_sample(logits: torch.Tensor, mask: torch.Tensor):
