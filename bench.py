@@ -594,6 +594,29 @@ def run_gpu_arm(args) -> int:
               "note": "policy forward + masked sampling + batched step + auto-reset, whole "
                       "horizon in one CUDA graph; observations written in place into the "
                       "[T+1,B,N,D] horizon buffer"}
+        if ro.policy is not None:
+            # the tcgen05 policy MLP alone on the rollout's own input (HBM-bound:
+            # x read once + 16 B of logits per agent row), timed on its stream
+            xin = ro._xin
+            rows = xin.shape[0] * xin.shape[1]
+            with cx.torch.cuda.stream(cx.stream):
+                for _ in range(3):
+                    ro.policy(xin)
+                m0, m1 = cx.event(), cx.event()
+                m0.record(cx.stream)
+                for _ in range(20):
+                    ro.policy(xin)
+                m1.record(cx.stream)
+            cx.stream.synchronize()
+            mlp_ms = m0.elapsed_time(m1) / 20
+            mlp_bytes = rows * (ro.policy.in_dim * 2 + 16)
+            peak = load_peaks().get("hbm_gbs", 6547.5)
+            c5["policy_mlp"] = {
+                "kernel": "mlp_policy_tma_kernel (tcgen05.mma M128 N128, TMA, TMEM accumulators)",
+                "us_avg": round(mlp_ms * 1000.0, 2), "rows": rows, "k": ro.policy.in_dim,
+                "bound": "hbm", "achieved_gbps": round(mlp_bytes / (mlp_ms / 1000.0) / 1e9, 1),
+                "peak_gbps": peak, "frac": round(mlp_bytes / (mlp_ms / 1000.0) / 1e9 / peak, 3),
+                "algorithmic_bytes": mlp_bytes}
         ro.close()
         del ro
         cx.torch.cuda.empty_cache()
