@@ -6,21 +6,19 @@
 // never leaves the SM (TMEM -> registers), so HBM sees x once and 16 B of
 // logits per row.
 //
-// Per CTA (persistent, one per SM, 128 threads):
-//   * 128-row tiles of x; the K dimension in chunks of 80 features.  Each
-//     chunk's x rows and W1 rows (W1 is L2-resident) are staged with
-//     cp.async (zero-filled past K and past the last row) into the canonical
-//     no-swizzle K-major UMMA layout: 8-row x 16-byte core matrices, core
-//     matrices adjacent in K 128 B apart (LBO), 8-row groups 1,280 B apart
-//     (SBO).  Five stages: a whole tile's chunks are in flight at once.
-//   * thread 0 issues tcgen05.mma.cta_group::1.kind::f16 (M = 128, N = 128,
-//     K = 16; five per chunk) into a 128-column fp32 TMEM accumulator and
-//     commits each chunk to that stage's mbarrier (frees the stage) and the
-//     tile's last chunk to the accumulator barrier.
-//   * epilogue: warp w reads TMEM lanes 32w..32w+31 (its rows) with
-//     tcgen05.ld 32x32b.x32, adds b1, ReLU, rounds to bf16 (the reference
-//     policy's hidden dtype), and contracts with W2 (fp32 copy in shared
-//     memory, broadcast reads) into the 8 logits; one 16-byte store per row.
+// Two kernels (tabx_policy_mlp picks by K):
+//   * mlp_policy_tma_kernel (K <= 704, the rollout's shapes): TMA-fed,
+//     warp-specialised, W1 resident in shared memory; see its comment below.
+//   * mlp_policy_kernel (larger K, where W1 does not fit beside the x
+//     stages): 128 threads per CTA stage each K chunk of 80 features of x and
+//     W1 with cp.async (zero-filled past K and past the last row) into the
+//     no-swizzle K-major UMMA layout (8-row x 16-byte core matrices, LBO
+//     128 B along K, SBO 1,280 B between 8-row groups), thread 0 issues the
+//     MMAs, the same threads run the epilogue.
+// Both share the epilogue (mlp_epilogue_cols): tcgen05.ld 32x32b.x32 of the
+// accumulator rows, + b1, ReLU, bf16 rounding (the module's hidden dtype),
+// times W2 (fp32 copy in shared memory, broadcast reads) into 8 logits; one
+// 16-byte store per row.
 #include <cuda_bf16.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -291,16 +289,23 @@ __global__ void __launch_bounds__(MLP_THREADS, 1)
 // reads: rows 128 B apart, 8-row groups 1,024 B apart, K advanced by 32 B
 // per 16-feature MMA inside the swizzle atom); the TMA unit zero-fills past
 // K and past the last row.  W1 is loaded once per CTA (every SM re-reading
-// W1 chunks from L2 each tile is a hot spot).  Roles: warps 0-3 epilogue
-// (TMEM lanes 32w..), warp 4 lane 0 issues the TMA loads, warp 5 lane 0 the
-// MMAs.  Two TMEM accumulators (256 columns): the epilogue of tile t
-// overlaps the MMAs of tile t + 1.
-constexpr int MLPT_THREADS = 320;  // 8 epilogue warps, TMA warp, MMA warp
+// W1 chunks from L2 each tile is a hot spot).  Roles: MLP_EW epilogue warps
+// (warp w reads TMEM lanes 32 (w % 4).. and hidden slice w / 4; slices are
+// summed through shared memory), then one warp whose lane 0 issues the TMA
+// loads and one whose lane 0 issues the MMAs.  Two TMEM accumulators (256
+// columns): the epilogue of tile t overlaps the MMAs of tile t + 1.
+#ifndef MLP_EW
+#define MLP_EW 16
+#endif
+constexpr int MLPT_EW = MLP_EW;                 // epilogue warps (4 per TMEM sub-partition)
+constexpr int MLPT_PARTS = MLPT_EW / 4;         // hidden-unit slices per row
+constexpr int MLPT_THREADS = 32 * (MLPT_EW + 2);  // + TMA warp + MMA warp
 constexpr int MLPT_KB = 64;                     // features per box / chunk
 constexpr int MLPT_BOX = MLP_M * MLPT_KB * 2;   // 16,384 B
 constexpr int MLPT_SMEM_MAX = 232448;           // 227 KB opt-in per CTA
 constexpr int MLPT_MISC =
-    MLP_H * MLP_OUT * 4 + MLP_H * 4 + MLP_OUT * 4 + 2 * MLP_M * MLP_OUT * 4 + 32 * 8 + 16 + 1024;
+    MLP_H * MLP_OUT * 4 + MLP_H * 4 + MLP_OUT * 4 + 2 * (MLPT_PARTS - 1) * MLP_M * MLP_OUT * 4 +
+    32 * 8 + 16 + 1024;
 
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t addr) {
   return (uint64_t)((addr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) |
@@ -337,9 +342,10 @@ __global__ void __launch_bounds__(MLPT_THREADS, 1)
   float* w2s = reinterpret_cast<float*>(sm + (size_t)(nch + nstages) * MLPT_BOX);
   float* b1s = w2s + MLP_H * MLP_OUT;
   float* b2s = b1s + MLP_H;
-  float* red = b2s + MLP_OUT;  // [2][128][8] partial logits of the upper column half
+  float* red = b2s + MLP_OUT;  // [2][PARTS-1][128][8] partial logits of slices 1..
   uint64_t* bars = reinterpret_cast<uint64_t*>(
-      (reinterpret_cast<uintptr_t>(red + 2 * MLP_M * MLP_OUT) + 7) & ~(uintptr_t)7);
+      (reinterpret_cast<uintptr_t>(red + 2 * (MLPT_PARTS - 1) * MLP_M * MLP_OUT) + 7) &
+      ~(uintptr_t)7);
   uint64_t* full = bars;          // [nstages]  x box landed (TMA bytes)
   uint64_t* empty = bars + 8;     // [nstages]  MMAs done reading it
   uint64_t* acc_full = bars + 16; // [2]
@@ -361,7 +367,8 @@ __global__ void __launch_bounds__(MLPT_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&acc_full[a])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 256;" ::"r"(smem_u32(&acc_empty[a])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&acc_empty[a])),
+                   "n"(32 * MLPT_EW));
     }
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(wfull)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(MLPT_THREADS, 1)
 
   // stage / phase counters advance incrementally: these two loops are single
   // threads whose instruction latency bounds the whole pipeline
-  if (warp == 8) {  // ---- TMA producer
+  if (warp == MLPT_EW) {  // ---- TMA producer
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tx)) : "memory");
       mbar_expect(smem_u32(wfull), (uint32_t)nch * MLPT_BOX);
@@ -409,7 +416,7 @@ __global__ void __launch_bounds__(MLPT_THREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp == 9) {  // ---- MMA issuer
+  } else if (warp == MLPT_EW + 1) {  // ---- MMA issuer
     if (lane == 0) {
       mbar_wait(smem_u32(wfull), 0u);
       const uint64_t da0 = umma_desc_sw128(stage0), db0 = umma_desc_sw128(w1a);
@@ -453,31 +460,38 @@ __global__ void __launch_bounds__(MLPT_THREADS, 1)
       }
     }
     __syncwarp();
-  } else {  // ---- epilogue: warp w -> TMEM lanes 32 (w % 4).., hidden half w / 4
-    const int sub = warp & 3, half = warp >> 2;
+  } else {  // ---- epilogue: warp w -> TMEM lanes 32 (w % 4).., hidden slice w / 4
+    constexpr int HS = MLP_H / MLPT_PARTS;  // hidden units per slice
+    const int sub = warp & 3, part = warp >> 2;
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int a = (int)(it & 1);
       mbar_wait(smem_u32(&acc_full[a]), (uint32_t)((it / 2) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float lg[MLP_OUT];
 #pragma unroll
-      for (int o = 0; o < MLP_OUT; ++o) lg[o] = half ? 0.0f : b2s[o];
-      mlp_epilogue_cols<MLP_H / 64>(
-          tmem + ((uint32_t)(sub * 32) << 16) + (uint32_t)(a * MLP_H + half * (MLP_H / 2)),
-          half * (MLP_H / 2), w2s, b1s, lg, smem_u32(&acc_empty[a]));
-      float* rr = red + ((size_t)a * MLP_M + sub * 32 + lane) * MLP_OUT;
-      if (half) {
+      for (int o = 0; o < MLP_OUT; ++o) lg[o] = part ? 0.0f : b2s[o];
+      mlp_epilogue_cols<HS / 32>(
+          tmem + ((uint32_t)(sub * 32) << 16) + (uint32_t)(a * MLP_H + part * HS), part * HS,
+          w2s, b1s, lg, smem_u32(&acc_empty[a]));
+      const int r = sub * 32 + lane;
+      if (part) {
+        float* rr = red + (((size_t)a * (MLPT_PARTS - 1) + part - 1) * MLP_M + r) * MLP_OUT;
         *reinterpret_cast<float4*>(rr) = make_float4(lg[0], lg[1], lg[2], lg[3]);
         *reinterpret_cast<float4*>(rr + 4) = make_float4(lg[4], lg[5], lg[6], lg[7]);
       }
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + sub) : "memory");  // the warp pair
-      if (!half) {
-        const float4 u = *reinterpret_cast<const float4*>(rr);
-        const float4 w = *reinterpret_cast<const float4*>(rr + 4);
-        lg[0] += u.x; lg[1] += u.y; lg[2] += u.z; lg[3] += u.w;
-        lg[4] += w.x; lg[5] += w.y; lg[6] += w.z; lg[7] += w.w;
+      // the warps of this sub-partition (one per slice)
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + sub), "n"(32 * MLPT_PARTS) : "memory");
+      if (!part) {
+#pragma unroll
+        for (int q = 1; q < MLPT_PARTS; ++q) {
+          const float* rr = red + (((size_t)a * (MLPT_PARTS - 1) + q - 1) * MLP_M + r) * MLP_OUT;
+          const float4 u = *reinterpret_cast<const float4*>(rr);
+          const float4 w = *reinterpret_cast<const float4*>(rr + 4);
+          lg[0] += u.x; lg[1] += u.y; lg[2] += u.z; lg[3] += u.w;
+          lg[4] += w.x; lg[5] += w.y; lg[6] += w.z; lg[7] += w.w;
+        }
         const int64_t tile = blockIdx.x + it * gridDim.x;
-        const int64_t row = tile * MLP_M + sub * 32 + lane;
+        const int64_t row = tile * MLP_M + r;
         if (row < rows) store_logits(out, row, lg);
       }
     }
