@@ -434,6 +434,18 @@ int tabx_policy_mlp(const void* x, int64_t rows, int32_t k, int64_t ldx, const v
                     const void* b1, const void* w2, const void* b2, void* logits, void* stream);
 
 /*
+ * tabx_policy_mlp with the masked sampler (tabx_masked_sample semantics, on
+ * the bfloat16 logits) fused into its epilogue: actions / logp per row from
+ * mask [rows, 7] and the noise counter (seed, *step_ptr + step_add).  logits
+ * may be NULL (not written) when k <= 704; larger k needs the buffer (the
+ * sampler then runs as a second kernel).  Asynchronous on `stream`.
+ */
+int tabx_policy_mlp_sample(const void* x, int64_t rows, int32_t k, int64_t ldx, const void* w1,
+                           const void* b1, const void* w2, const void* b2, void* logits,
+                           const uint8_t* mask, uint64_t seed, const uint64_t* step_ptr,
+                           uint64_t step_add, int64_t* actions, float* logp, void* stream);
+
+/*
  * Tool hook: SM cycles per step phase summed over envs (all step kernels),
  * nonzero only in a build with -DTABX_PHASE_PROF (tools/phase_prof.py).
  */

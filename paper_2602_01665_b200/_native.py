@@ -146,6 +146,8 @@ def lib() -> ct.CDLL:
         "tabx_debug_sincos": (_i32, [P, P, P, _i64, P]),
         "tabx_pack_bf16": (_i32, [P, _i64, _i32, _i32, P, P]),
         "tabx_policy_mlp": (_i32, [P, _i64, _i32, _i64, P, P, P, P, P, P]),
+        "tabx_policy_mlp_sample": (_i32, [P, _i64, _i32, _i64, P, P, P, P, P, P, ct.c_uint64, P,
+                                          ct.c_uint64, P, P, P]),
         "tabx_masked_sample": (_i32, [P, _i32, _i64, P, _i64, ct.c_uint64, P, ct.c_uint64, P, P,
                                       P]),
         "tabx_debug_phase_cycles": (_i32, [P, _i32]),

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "tabx_device.cuh"
+#include "tabx_sample.cuh"
 
 namespace tabx {
 cudaError_t launch_lanes(const Params& P, int W, int sm_count, cudaStream_t stream, int* grid);
@@ -19,9 +20,10 @@ cudaError_t launch_ctrl(const Params& P, int W, int nh, int sm_count, cudaStream
 cudaError_t launch_emit(const Params& P, int W, int sm_count, cudaStream_t stream);
 cudaError_t launch_fused_w1(const Params& P, int variant, int sm_count, cudaStream_t stream);
 cudaError_t launch_small_w1(const Params& P, int sm_count, cudaStream_t stream);
+bool mlp_fused_sampling(int K);
 cudaError_t launch_mlp_policy(const void* x, int64_t rows, int K, int64_t ldx, const void* w1,
                               const void* b1, const void* w2, const void* b2, void* out,
-                              int sm_count, cudaStream_t stream);
+                              const MlpSample& sa, int sm_count, cudaStream_t stream);
 cudaError_t launch_validate(const int64_t* actions, const DevState& st, const tabx_config* cfgs,
                             int64_t B, int N, Sync* sync, int sm_count, cudaStream_t stream);
 cudaError_t launch_spawn(const DevState& st, const tabx_config* cfgs, const DerivedCfg* dcfgs,
@@ -974,8 +976,30 @@ int tabx_policy_mlp(const void* x, int64_t rows, int32_t k, int64_t ldx, const v
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  TABX_CUDA(launch_mlp_policy(x, rows, k, ldx, w1, b1, w2, b2, logits, sms, (cudaStream_t)stream),
+  const MlpSample none{nullptr, 0, nullptr, 0, nullptr, nullptr};
+  TABX_CUDA(launch_mlp_policy(x, rows, k, ldx, w1, b1, w2, b2, logits, none, sms,
+                              (cudaStream_t)stream),
             "policy mlp");
+  return TABX_OK;
+}
+
+int tabx_policy_mlp_sample(const void* x, int64_t rows, int32_t k, int64_t ldx, const void* w1,
+                           const void* b1, const void* w2, const void* b2, void* logits,
+                           const uint8_t* mask, uint64_t seed, const uint64_t* step_ptr,
+                           uint64_t step_add, int64_t* actions, float* logp, void* stream) {
+  if (rows < 0 || k < 8 || (k & 7) || ldx < k || (ldx & 7) ||
+      (rows > 0 && (!x || !w1 || !b1 || !w2 || !b2 || !mask || !actions || !logp)) ||
+      (((uintptr_t)x | (uintptr_t)w1 | (uintptr_t)logits) & 15))
+    return fail(TABX_E_ARGUMENT, "tabx_policy_mlp_sample: bad argument");
+  if (!logits && !mlp_fused_sampling(k))
+    return fail(TABX_E_ARGUMENT, "tabx_policy_mlp_sample: this k needs a logits buffer");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const MlpSample sa{mask, seed, step_ptr, step_add, actions, logp};
+  TABX_CUDA(launch_mlp_policy(x, rows, k, ldx, w1, b1, w2, b2, logits, sa, sms,
+                              (cudaStream_t)stream),
+            "policy mlp + sample");
   return TABX_OK;
 }
 

@@ -28,6 +28,7 @@
 #include <mutex>
 
 #include "tabx_device.cuh"
+#include "tabx_sample.cuh"
 
 namespace tabx {
 
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(MLPT_THREADS, 1)
                           const __nv_bfloat16* __restrict__ b1,
                           const __nv_bfloat16* __restrict__ w2,
                           const __nv_bfloat16* __restrict__ b2, __nv_bfloat16* __restrict__ out,
-                          int nstages) {
+                          int nstages, const MlpSample sa) {
   extern __shared__ __align__(1024) unsigned char sm_raw[];
   const uint32_t raw = smem_u32(sm_raw);
   unsigned char* sm = sm_raw + (((raw + 1023u) & ~1023u) - raw);  // 1,024-B aligned
@@ -463,6 +464,7 @@ __global__ void __launch_bounds__(MLPT_THREADS, 1)
   } else {  // ---- epilogue: warp w -> TMEM lanes 32 (w % 4).., hidden slice w / 4
     constexpr int HS = MLP_H / MLPT_PARTS;  // hidden units per slice
     const int sub = warp & 3, part = warp >> 2;
+    const uint64_t skey = sa.mask ? sample_key(sa.seed, sa.step_ptr, sa.step_add) : 0ull;
     for (int64_t it = 0; it < my_tiles; ++it) {
       const int a = (int)(it & 1);
       mbar_wait(smem_u32(&acc_full[a]), (uint32_t)((it / 2) & 1));
@@ -492,7 +494,19 @@ __global__ void __launch_bounds__(MLPT_THREADS, 1)
         }
         const int64_t tile = blockIdx.x + it * gridDim.x;
         const int64_t row = tile * MLP_M + r;
-        if (row < rows) store_logits(out, row, lg);
+        if (row < rows) {
+          __align__(16) __nv_bfloat16 ob[MLP_OUT];
+#pragma unroll
+          for (int o = 0; o < MLP_OUT; ++o) ob[o] = __float2bfloat16_rn(lg[o]);
+          if (out)
+            *reinterpret_cast<uint4*>(out + row * MLP_OUT) = *reinterpret_cast<const uint4*>(ob);
+          if (sa.mask) {  // the sampler on the bf16 logits, as the stand-alone kernel reads them
+            float lv[TABX_NUM_ACTIONS];
+#pragma unroll
+            for (int o = 0; o < TABX_NUM_ACTIONS; ++o) lv[o] = __bfloat162float(ob[o]);
+            sample_row(lv, sa.mask + row * TABX_NUM_ACTIONS, skey, row, sa.actions, sa.logp);
+          }
+        }
       }
     }
   }
@@ -533,14 +547,28 @@ static bool encode_rows(CUtensorMap* m, const void* base, int64_t rows, int K, i
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+cudaError_t launch_masked_sample(const void* logits, int bf16, int64_t ld, const uint8_t* mask,
+                                 int64_t M, uint64_t seed, const uint64_t* step_ptr,
+                                 uint64_t step_add, int64_t* actions, float* logp, int sm_count,
+                                 cudaStream_t stream);
+
+static int mlp_tma_stages(int K) {
+  const int nch = (K + MLPT_KB - 1) / MLPT_KB;
+  return (MLPT_SMEM_MAX - MLPT_MISC) / MLPT_BOX - nch;
+}
+
+// The fused sampler runs in the TMA kernel; the W1-streaming kernel (large K)
+// needs a logits buffer and a separate sampler pass.
+bool mlp_fused_sampling(int K) { return mlp_tma_stages(K) >= 3; }
+
 cudaError_t launch_mlp_policy(const void* x, int64_t rows, int K, int64_t ldx, const void* w1,
                               const void* b1, const void* w2, const void* b2, void* out,
-                              int sm_count, cudaStream_t stream) {
+                              const MlpSample& sa, int sm_count, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   const int64_t ntiles = (rows + MLP_M - 1) / MLP_M;
   const int grid = (int)(ntiles < sm_count ? ntiles : sm_count);
   const int nch = (K + MLPT_KB - 1) / MLPT_KB;
-  const int tma_stages = (MLPT_SMEM_MAX - MLPT_MISC) / MLPT_BOX - nch;
+  const int tma_stages = mlp_tma_stages(K);
   int per_sm = 0;  // (launch_geometry sets the shared-memory attribute once per device)
   CUtensorMap tx, tw;
   if (tma_stages >= 3 && encode_rows(&tx, x, rows, K, ldx) && encode_rows(&tw, w1, MLP_H, K, K)) {
@@ -551,16 +579,20 @@ cudaError_t launch_mlp_policy(const void* x, int64_t rows, int K, int64_t ldx, c
     if (e != cudaSuccess) return e;
     mlp_policy_tma_kernel<<<grid, MLPT_THREADS, smem, stream>>>(
         tx, tw, rows, K, (const __nv_bfloat16*)b1, (const __nv_bfloat16*)w2,
-        (const __nv_bfloat16*)b2, (__nv_bfloat16*)out, ns);
+        (const __nv_bfloat16*)b2, (__nv_bfloat16*)out, ns, sa);
     return cudaGetLastError();
   }
+  if (!out) return cudaErrorInvalidValue;  // (the C ABI rejects this case first)
   cudaError_t e = launch_geometry((const void*)mlp_policy_kernel, MLP_THREADS, MLP_SMEM, &per_sm);
   if (e != cudaSuccess) return e;
   mlp_policy_kernel<<<grid, MLP_THREADS, MLP_SMEM, stream>>>(
       (const __nv_bfloat16*)x, rows, K, ldx, (const __nv_bfloat16*)w1,
       (const __nv_bfloat16*)b1, (const __nv_bfloat16*)w2, (const __nv_bfloat16*)b2,
       (__nv_bfloat16*)out);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess || !sa.mask) return e;
+  return launch_masked_sample(out, 1, MLP_OUT, sa.mask, rows, sa.seed, sa.step_ptr, sa.step_add,
+                              sa.actions, sa.logp, sm_count, stream);
 }
 
 }  // namespace tabx

@@ -9,14 +9,9 @@
 #include <stdint.h>
 
 #include "tabx_device.cuh"
+#include "tabx_sample.cuh"
 
 namespace tabx {
-
-__device__ __forceinline__ uint64_t sm_mix(uint64_t x) {
-  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
-  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
-  return x ^ (x >> 31);
-}
 
 template <typename T>
 __device__ __forceinline__ float load_logit(const T* p);
@@ -34,36 +29,14 @@ __global__ void masked_sample_kernel(const T* __restrict__ logits, int64_t ld,
                                      const uint8_t* __restrict__ mask, int64_t M, uint64_t seed,
                                      const uint64_t* __restrict__ step_ptr, uint64_t step_add,
                                      int64_t* __restrict__ actions, float* __restrict__ logp) {
-  const uint64_t step = (step_ptr ? *step_ptr : 0ull) + step_add;
-  const uint64_t key = sm_mix(seed + 0x9E3779B97F4A7C15ull * (step + 1));
+  const uint64_t key = sample_key(seed, step_ptr, step_add);
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < M;
        r += (int64_t)gridDim.x * blockDim.x) {
     const T* l = logits + r * ld;
-    const uint8_t* m = mask + r * TABX_NUM_ACTIONS;
-    float v[TABX_NUM_ACTIONS];
-    float mx = -INFINITY;
+    float lg[TABX_NUM_ACTIONS];
 #pragma unroll
-    for (int a = 0; a < TABX_NUM_ACTIONS; ++a) {
-      v[a] = m[a] ? load_logit<T>(l + a) : -INFINITY;
-      mx = fmaxf(mx, v[a]);
-    }
-    float se = 0.0f, best = -INFINITY;
-    int arg = TABX_NUM_ACTIONS - 1;
-    const uint64_t h = sm_mix(key ^ (uint64_t)r * 0xD1B54A32D192ED03ull);
-#pragma unroll
-    for (int a = 0; a < TABX_NUM_ACTIONS; ++a) {
-      if (v[a] == -INFINITY) continue;
-      se += __expf(v[a] - mx);
-      const uint64_t z = sm_mix(h + (uint64_t)(a + 1) * 0x9E3779B97F4A7C15ull);
-      const float u = ((float)(z >> 40) + 0.5f) * (1.0f / 16777216.0f);  // (0, 1)
-      const float g = v[a] - __logf(-__logf(u));
-      if (g > best) {
-        best = g;
-        arg = a;
-      }
-    }
-    actions[r] = arg;
-    logp[r] = v[arg] - mx - __logf(se);
+    for (int a = 0; a < TABX_NUM_ACTIONS; ++a) lg[a] = load_logit<T>(l + a);
+    sample_row(lg, mask + r * TABX_NUM_ACTIONS, key, r, actions, logp);
   }
 }
 

@@ -10,8 +10,8 @@ once into a CUDA graph and replayed per iteration.
 Policies: ``random`` (uniform over legal actions, the reference's random
 controller semantics) or ``mlp`` (a bf16 two-layer MLP over the per-agent
 observation).  Either way the actions come from the library's fused masked
-Gumbel-max sampler (``tabx_masked_sample``: one pass per agent producing the
-action and its log-probability, noise keyed on a device step counter so the
+Gumbel-max sampler (``tabx_masked_sample``, fused into the policy-MLP kernel
+for ``mlp``: one pass per agent producing the action and its log-probability, noise keyed on a device step counter so the
 replayed graph draws fresh noise).  The MLP reads a bf16 copy of the
 observation padded to a multiple of 8 features (aligned GEMM rows) and emits
 8 logits of which the first 7 are the actions.  The ally team is driven by
@@ -160,16 +160,22 @@ class Rollout:
         mask = self.sim._buf["action_mask"]
         L = nat.lib()
         stream = torch.cuda.current_stream(self.device).cuda_stream
+        ptr = lambda x: ct.c_void_p(x.data_ptr())  # noqa: E731
         if self.policy is None:
-            logits, bf16 = self._zero_logits, 0
+            logits = self._zero_logits
+            nat.check(L.tabx_masked_sample(
+                ptr(logits), 0, logits.shape[-1], ptr(mask), self.B * self.N,
+                ct.c_uint64(self.seed), ptr(self._ctr), t, ptr(self.buf.actions[t]),
+                ptr(self.buf.logp[t]), ct.c_void_p(stream)), "tabx_masked_sample")
         else:
-            # _xin: the current observation in bf16, written by the last step
-            logits, bf16 = self.policy(self._xin).reshape(self.B * self.N, -1), 1
-        nat.check(L.tabx_masked_sample(
-            ct.c_void_p(logits.data_ptr()), bf16, logits.shape[-1], ct.c_void_p(mask.data_ptr()),
-            self.B * self.N, ct.c_uint64(self.seed), ct.c_void_p(self._ctr.data_ptr()), t,
-            ct.c_void_p(self.buf.actions[t].data_ptr()), ct.c_void_p(self.buf.logp[t].data_ptr()),
-            ct.c_void_p(stream)), "tabx_masked_sample")
+            # _xin: the current observation in bf16, written by the last step;
+            # policy MLP + masked sampler in one tcgen05 kernel (no logits in HBM)
+            p = self.policy
+            nat.check(L.tabx_policy_mlp_sample(
+                ptr(self._xin), self.B * self.N, p.in_dim, p.in_dim, ptr(p.l1.weight),
+                ptr(p.l1.bias), ptr(p.l2.weight), ptr(p.l2.bias), None, ptr(mask),
+                ct.c_uint64(self.seed), ptr(self._ctr), t, ptr(self.buf.actions[t]),
+                ptr(self.buf.logp[t]), ct.c_void_p(stream)), "tabx_policy_mlp_sample")
         nat.check(L.tabx_step(self.sim.handle, ct.c_void_p(self.buf.actions[t].data_ptr()),
                               ct.byref(self._outs[t])), "tabx_step")
 

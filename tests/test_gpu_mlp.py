@@ -59,3 +59,40 @@ def test_policy_mlp_rejects_bad_shapes():
     pol = MLPPolicy(386, hidden=64).cuda().bfloat16()
     with pytest.raises(ValueError):
         pol(torch.zeros(4, 392, device="cuda", dtype=torch.bfloat16))
+
+
+@pytest.mark.parametrize("rows", [1, 130, 20000])
+def test_fused_sampler_equals_mlp_then_sampler(rows):
+    """tabx_policy_mlp_sample (sampler fused into the MLP epilogue) draws the
+    same actions and log-probabilities, bit for bit, as the MLP kernel
+    followed by the stand-alone tabx_masked_sample on its bf16 logits."""
+    import ctypes as ct
+
+    from paper_2602_01665_b200 import _native as nat
+    torch.manual_seed(rows)
+    pol = MLPPolicy(386).cuda().bfloat16()
+    x = torch.randn(rows, pol.in_dim, device="cuda").bfloat16()
+    mask = (torch.rand(rows, 7, device="cuda") < 0.6).to(torch.uint8)
+    mask[:, 0] = 1  # at least one legal action per row
+    ctr = torch.tensor([5], dtype=torch.int64, device="cuda")
+    L, s = nat.lib(), ct.c_void_p(torch.cuda.current_stream().cuda_stream)
+    p = lambda t: ct.c_void_p(t.data_ptr())  # noqa: E731
+    a1 = torch.empty(rows, dtype=torch.int64, device="cuda")
+    l1 = torch.empty(rows, device="cuda")
+    logits = pol(x)
+    nat.check(L.tabx_masked_sample(p(logits), 1, 8, p(mask), rows, ct.c_uint64(77), p(ctr), 3,
+                                   p(a1), p(l1), s), "sample")
+    a2, l2 = torch.empty_like(a1), torch.empty_like(l1)
+    lg2 = torch.empty_like(logits)
+    nat.check(L.tabx_policy_mlp_sample(
+        p(x), rows, pol.in_dim, pol.in_dim, p(pol.l1.weight), p(pol.l1.bias), p(pol.l2.weight),
+        p(pol.l2.bias), p(lg2), p(mask), ct.c_uint64(77), p(ctr), 3, p(a2), p(l2), s), "fused")
+    a3, l3 = torch.empty_like(a1), torch.empty_like(l1)
+    nat.check(L.tabx_policy_mlp_sample(
+        p(x), rows, pol.in_dim, pol.in_dim, p(pol.l1.weight), p(pol.l1.bias), p(pol.l2.weight),
+        p(pol.l2.bias), None, p(mask), ct.c_uint64(77), p(ctr), 3, p(a3), p(l3), s), "fused")
+    torch.cuda.synchronize()
+    assert torch.equal(lg2, logits)
+    assert torch.equal(a1, a2) and torch.equal(a1, a3)
+    assert torch.equal(l1, l2) and torch.equal(l1, l3)
+    assert bool((mask.gather(1, a1[:, None]) == 1).all())  # only legal actions

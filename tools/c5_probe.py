@@ -23,3 +23,13 @@ print("mlp forward  ", round(t(lambda: ro.policy(ro._xin)), 4), "ms")
 print("one step     ", round(t(lambda: ro._step(0)), 4), "ms")
 ro.run()
 print("horizon/16   ", round(t(lambda: ro.run(), 3) / 16, 4), "ms (graph replay)")
+logits = ro.policy(ro._xin).reshape(B * ro.N, -1)
+L = nat.lib()
+def sample():
+    L.tabx_masked_sample(ct.c_void_p(logits.data_ptr()), 1, 8, ct.c_void_p(mask.data_ptr()), B * ro.N,
+                         ct.c_uint64(0), None, 0, ct.c_void_p(ro.buf.actions[0].data_ptr()),
+                         ct.c_void_p(ro.buf.logp[0].data_ptr()), ct.c_void_p(torch.cuda.current_stream().cuda_stream))
+print("sampler      ", round(t(sample), 4), "ms")
+def envstep():
+    L.tabx_step(ro.sim.handle, ct.c_void_p(ro.buf.actions[0].data_ptr()), ct.byref(ro._outs[0]))
+print("env step     ", round(t(envstep), 4), "ms")
