@@ -595,25 +595,39 @@ def run_gpu_arm(args) -> int:
                       "horizon in one CUDA graph; observations written in place into the "
                       "[T+1,B,N,D] horizon buffer"}
         if ro.policy is not None:
-            # the tcgen05 policy MLP alone on the rollout's own input (HBM-bound:
-            # x read once + 16 B of logits per agent row), timed on its stream
-            xin = ro._xin
+            # the rollout's policy kernel alone (tcgen05 MLP + fused masked
+            # sampler, tabx_policy_mlp_sample) on the rollout's own input and
+            # mask: HBM-bound, x read once, mask in, action + log-prob out
+            import ctypes as _ct
+            from paper_2602_01665_b200 import _native as _nat
+            pol, xin = ro.policy, ro._xin
             rows = xin.shape[0] * xin.shape[1]
-            with cx.torch.cuda.stream(cx.stream):
-                for _ in range(3):
-                    ro.policy(xin)
-                m0, m1 = cx.event(), cx.event()
-                m0.record(cx.stream)
-                for _ in range(20):
-                    ro.policy(xin)
-                m1.record(cx.stream)
+            mask = ro.sim._buf["action_mask"]
+            act, lp = ro.buf.actions[0], ro.buf.logp[0]
+            ptr = lambda t: _ct.c_void_p(t.data_ptr())  # noqa: E731
+            lib = _nat.lib()
+
+            def _pol():
+                lib.tabx_policy_mlp_sample(
+                    ptr(xin), rows, pol.in_dim, pol.in_dim, ptr(pol.l1.weight),
+                    ptr(pol.l1.bias), ptr(pol.l2.weight), ptr(pol.l2.bias), None, ptr(mask),
+                    _ct.c_uint64(0), None, 0, ptr(act), ptr(lp),
+                    _ct.c_void_p(cx.stream.cuda_stream))
+            for _ in range(3):
+                _pol()
+            m0, m1 = cx.event(), cx.event()
+            m0.record(cx.stream)
+            for _ in range(20):
+                _pol()
+            m1.record(cx.stream)
             cx.stream.synchronize()
             mlp_ms = m0.elapsed_time(m1) / 20
-            mlp_bytes = rows * (ro.policy.in_dim * 2 + 16)
+            mlp_bytes = rows * (pol.in_dim * 2 + 7 + 8 + 4)
             peak = load_peaks().get("hbm_gbs", 6547.5)
             c5["policy_mlp"] = {
-                "kernel": "mlp_policy_tma_kernel (tcgen05.mma M128 N128, TMA, TMEM accumulators)",
-                "us_avg": round(mlp_ms * 1000.0, 2), "rows": rows, "k": ro.policy.in_dim,
+                "kernel": "mlp_policy_tma_kernel (tcgen05.mma M128 N128 K16, TMA 128B-swizzled "
+                          "boxes, TMEM accumulators) with the masked sampler in its epilogue",
+                "us_avg": round(mlp_ms * 1000.0, 2), "rows": rows, "k": pol.in_dim,
                 "bound": "hbm", "achieved_gbps": round(mlp_bytes / (mlp_ms / 1000.0) / 1e9, 1),
                 "peak_gbps": peak, "frac": round(mlp_bytes / (mlp_ms / 1000.0) / 1e9 / peak, 3),
                 "algorithmic_bytes": mlp_bytes}
