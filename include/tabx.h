@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define TABX_ABI_VERSION 5
+#define TABX_ABI_VERSION 6
 
 #define TABX_MAX_UNITS 256
 #define TABX_MAX_ZONES 32

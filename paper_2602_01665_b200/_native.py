@@ -12,7 +12,7 @@ MAX_UNITS = 256
 MAX_ZONES = 32
 NUM_ACTIONS = 7
 NUM_STATS = 8
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 OK = 0
 E_ARGUMENT, E_CUDA, E_ACTION_MASK, E_SHAPE, E_ALIGNMENT, E_CAPACITY = 1, 2, 3, 4, 5, 6
